@@ -1,0 +1,354 @@
+"""ADMM reconstruction throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one ADMM iteration (5 CG iterations: 5 forward + 5 adjoint NUDFTs,
+stencils, soft thresholds, CG/ADMM updates) of BASELINE config C (default 1:
+128x128, 8 coils, 64x256 golden-angle samples) on seeded synthetic inputs.
+``value`` = ADMM iterations/s over the K timed iterations, device time
+(CUDA events) of the native loop with inputs resident in HBM and L2 flushed
+between iterations (256 MiB overwrite, outside the timed intervals), max
+over ranks.  ``e2e`` = the same metric through the public API
+(``admm_reconstruct`` with pinned host arrays: plan build, H2D, full
+reconstruction of the config's iteration count, D2H of the image).
+Multi-GPU (torchrun): coils are sharded across ranks, one NCCL allreduce of
+the image partial per CG iteration; total work is fixed -> strong scaling.
+``--impl reference`` times the CPU arm (the numpy restatement of the
+reference in oracle/, f64, all host threads) on the same config and metric.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from harness.configs import CONFIGS, make_problem, nudft_flops_per_cg  # noqa: E402
+
+PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+METRIC = "ADMM iters/s"
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except (OSError, ValueError):
+        return FALLBACK_PEAKS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun")
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def pinned(arr):
+    import torch
+    t = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0].copy()).dtype, pin_memory=True)
+    t.numpy()[...] = arr
+    return t.numpy()
+
+
+# --------------------------------------------------------------------------
+def cpu_arm_rate(prob, n_iters):
+    """Oracle (numpy restatement of the reference, f64) ADMM it/s over
+    n_iters iterations with all host threads; returns (rate, seconds)."""
+    from oracle import csrecon_oracle as O
+    params = O.Params(**dict(prob.params, admm_max_iters=n_iters))
+    op = O.Operator(prob.coords, prob.sens, prob.n_frames, "double")
+    t0 = time.perf_counter()
+    O.admm(prob.data, prob.coords, prob.sens, params, "double", prob.n_frames, op=op)
+    dt = time.perf_counter() - t0
+    return n_iters / dt, dt
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return None
+    prob = make_problem(cfg)
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        cpu_arm_rate(prob, 1)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_arm_rate(prob, 1)
+        times.append(dt)
+    total = float(np.sum(times))
+    value = args.steps / total
+    sample = (f"config {cfg}: {args.steps} steps of 1 ADMM iteration (5 CG) each, "
+              f"f64 numpy/OpenBLAS oracle port of csrecon, {cores} threads")
+    return {"metric": METRIC, "value": value, "unit": "iter/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded BASELINE generators)",
+            "config": config_dict(cfg, world),
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def config_dict(cfg, world):
+    c = CONFIGS[cfg]
+    m = c["spokes"] * c["readout"]
+    return {"workload": f"BASELINE config {cfg}: ADMM-CG recon {c['nx']}x{c['ny']}"
+                        f"{'x' + str(c['n_frames']) if c['n_frames'] > 1 else ''}, "
+                        f"{c['n_coils']} coils, {c['spokes']}x{c['readout']} golden-angle "
+                        f"samples/frame, CG=5",
+            "nx": c["nx"], "ny": c["ny"], "frames": c["n_frames"], "coils": c["n_coils"],
+            "samples_per_frame": m, "cg_iters": 5, "lam": c["lam"], "beta": c["beta"],
+            "parallelism": f"coil-shard x{world}" if world > 1 else "1 GPU",
+            "l2": "flushed between timed iterations (256 MiB overwrite)"}
+
+
+def time_kernels(op, prob, reps=20):
+    """Per-launch device time of the NUDFT forward and adjoint on resident
+    data (CUDA events on the launching stream)."""
+    import torch
+    from paper_2006_14080_b200 import _dev, _native
+    dev = op.device
+    st = _dev.stream_ptr(dev)
+    x = torch.from_numpy(np.ascontiguousarray(
+        np.broadcast_to(prob.truth, op.image_shape).astype(np.complex64))).to(dev)
+    y = torch.empty((op.n_samples, op.n_coils), dtype=torch.complex64, device=dev)
+    img = torch.empty(op.image_shape, dtype=torch.complex64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    res = {}
+    for name in ("forward", "adjoint"):
+        ms = []
+        for i in range(reps + 3):
+            flush.fill_(i & 255)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            if name == "forward":
+                _native.call("csr_forward", op.plan, x.data_ptr(), y.data_ptr(), st)
+            else:
+                _native.call("csr_adjoint", op.plan, y.data_ptr(), img.data_ptr(), st)
+            b.record()
+            b.synchronize()
+            if i >= 3:
+                ms.append(a.elapsed_time(b))
+        res[name] = float(np.mean(ms))
+    return res
+
+
+def run_ours(args, cfg, world, rank, local):
+    import ctypes
+
+    import torch
+
+    import paper_2006_14080_b200 as P
+    from paper_2006_14080_b200 import _native
+    from paper_2006_14080_b200.solver import _Shard
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prob = make_problem(cfg)
+    traj = P.Trajectory(prob.coords, prob.coords.shape[0], 1)
+    ds = P.KSpaceDataset(prob.data, traj, n_frames=prob.n_frames)
+    base = P.ReconParams(**prob.params)
+    sh = _Shard(ds, prob.sens, world, "auto", dev)
+    op = sh.op
+    lib = _native.load()
+
+    def run(n_iters, iter_ms=None, flush=None):
+        params = P.ReconParams(**dict(prob.params, admm_max_iters=n_iters))
+        rho = torch.empty(op.image_shape, dtype=torch.complex64, device=dev)
+        log = (_native.IterLog * n_iters)()
+        stats = _native.RunStats()
+        if iter_ms is not None:
+            _native.call("csr_plan_set_timing", op.plan,
+                         flush.data_ptr() if flush is not None else None,
+                         flush.numel() if flush is not None else 0, iter_ms)
+        rc = lib.csr_admm_run(op.plan, ctypes.byref(params.native()), sh.data.data_ptr(),
+                              rho.data_ptr(), log, ctypes.byref(stats),
+                              torch.cuda.current_stream(dev).cuda_stream, None)
+        _native.check(rc)
+        _native.call("csr_plan_set_timing", op.plan, None, 0, None)
+        return stats
+
+    # warm-up (graph capture, clocks)
+    run(max(args.warmup, 3))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    iter_ms = (ctypes.c_float * args.steps)()
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    stats = run(args.steps, iter_ms, flush)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    t_solve = max_over_ranks(stats.solve_ms / 1e3, world)
+    value = args.steps / t_solve
+    kpi = stats.kernels_per_iter
+
+    # roofline: dominant kernel = the NUDFT GEMMs (forward / adjoint)
+    kt = time_kernels(op, prob)
+    flops_launch = 8.0 * op.n_coils * op.m_per_frame * op.nx * op.ny * op.n_frames
+    pk, src = peaks()
+    dom = max(kt, key=kt.get)
+    achieved = flops_launch / (kt[dom] * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": f"nudft_{dom}",
+                "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": None,
+                "peak_source": f"{src} dense bf16",
+                "flops_per_launch": flops_launch,
+                "ms_per_launch": kt,
+                "share_of_step": {k: 5 * v / (1e3 * t_solve / args.steps) for k, v in kt.items()}}
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    n_e2e = prob.params["admm_max_iters"]
+    data_p, sens_p = pinned(prob.data), pinned(prob.sens)
+    ds_p = P.KSpaceDataset(data_p, traj, n_frames=prob.n_frames)
+    e2e_times = []
+    for i in range(2):
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        img, rep = P.admm_reconstruct(ds_p, sens_p, base, n_workers=world,
+                                      compute_objectives=False, device=dev)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i > 0:
+            e2e_times.append(max_over_ranks(dt, world))
+    e2e = {"value": n_e2e / float(np.mean(e2e_times)), "unit": "iter/s",
+           "h2d_bytes_per_step": int(data_p.nbytes // world + sens_p.nbytes // world +
+                                     prob.coords.nbytes),
+           "d2h_bytes_per_step": int(img.nbytes),
+           "step": f"one admm_reconstruct call ({n_e2e} ADMM iterations, host in/out)"}
+
+    out = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * t_solve / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "c64 (3xTF32 tensor GEMM, "
+           "fp32 accumulate)" if op.info()["gemm_path"] == "tcgen05" else "c64 (fp32 SIMT)",
+           "data": "synthetic (seeded BASELINE generators; no public dataset)",
+           "config": config_dict(cfg, world), "clocks": clk, "e2e": e2e,
+           "gpu_launches": int(kpi * args.steps), "roofline": roofline,
+           "nudft_tflops": 5 * 2 * flops_launch / (1e3 * t_solve / args.steps) / 1e9,
+           "backend": op.info()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        rate, dt = cpu_arm_rate(prob, 2)
+        out["cpu_baseline"] = {"value": rate, "unit": "iter/s", "cores": cores,
+                               "kind": "port",
+                               "sample": f"config {cfg}, 2 ADMM iterations (5 CG each) of the "
+                                         f"f64 numpy oracle port, {dt:.1f} s"}
+    return out if rank == 0 else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        out = run_reference(args, args.config, world, rank)
+    else:
+        out = run_ours(args, args.config, world, rank, local)
+    if out is not None:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

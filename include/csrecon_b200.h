@@ -1,0 +1,191 @@
+/*
+ * csrecon_b200 — C ABI of the B200-native ADMM + NUDFT reconstruction path.
+ *
+ * Drop-in boundary for the reference package csrecon (/root/reference/pkg,
+ * Python).  The reference's plug-in point is its kernel table
+ * (kernels.py:212-231) behind DftOperator.forward/adjoint
+ * (operators.py:185-203), transform.theta/theta_adjoint/soft_threshold
+ * (transform.py:14-42), tensor.hermitian_dot/axpy (tensor.py:44-64) and the
+ * solver entry admm_reconstruct (solver.py:274-360).  Each entry point below
+ * names the reference interface it replaces.  The Python host package
+ * (paper_2006_14080_b200) binds these with ctypes; INTEGRATION.md shows the
+ * binding a csrecon maintainer would add.
+ *
+ * Conventions
+ *  - complex data are interleaved complex64 (float2), C-contiguous, in the
+ *    reference's index order: image (T, nx, ny) with pixel n = x*ny + y
+ *    (acquisition.py:15-43); k-space (T*M, C) sample-major, readout-major
+ *    rows (acquisition.py:46-53, 99-122).  T = 1 for the static problem.
+ *  - every buffer argument is caller-owned DEVICE memory unless documented
+ *    as host; the plan owns its factors and workspace.  Hot calls never
+ *    allocate.  Calls are ordered on the given stream (cudaStream_t passed
+ *    as void*; NULL = legacy default stream).
+ *  - a plan is bound to one device and is not re-entrant; different plans
+ *    may be driven from different threads.
+ *  - return value: CSR_OK or an error code; csr_last_error() gives the
+ *    thread-local message.  The host wrapper maps CSR_ERR_SHAPE to
+ *    ShapeMismatchError (tensor.py:17-18), CSR_ERR_NONFINITE to
+ *    CgDivergenceError (solver.py:30-31), CSR_ERR_OOM to MemoryBudgetError
+ *    (operators.py:26-27) and the rest to RuntimeError.
+ *  - there is no CPU fallback: without a usable sm_100 device every call
+ *    fails with CSR_ERR_CUDA.
+ */
+#ifndef CSRECON_B200_H
+#define CSRECON_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSR_OK 0
+#define CSR_ERR_SHAPE 1
+#define CSR_ERR_OOM 2
+#define CSR_ERR_CUDA 3
+#define CSR_ERR_NCCL 4
+#define CSR_ERR_NONFINITE 5
+#define CSR_ERR_ARG 6
+
+typedef struct csr_plan csr_plan;
+typedef struct csr_comm csr_comm;
+
+/* Geometry of one encoding operator (one worker's shard).  Replaces
+ * DftOperator.build(trajectory, grid, sens, mode, precision)
+ * (operators.py:141-164): coords are the (T*M, 2) cycles/pixel sample
+ * locations (host f64, Trajectory.coords, acquisition.py:46-73), sens the
+ * (C, nx, ny) coil maps (device complex64).  Frames t use rows
+ * [t*M, (t+1)*M).  Factors are generated on the device in f64 and rounded
+ * once to complex64, exactly as _unit_phase (operators.py:50-59). */
+typedef struct csr_plan_desc {
+    int32_t nx, ny;
+    int32_t n_frames;     /* T >= 1 */
+    int32_t n_coils;      /* C >= 1 (coils owned by this plan) */
+    int64_t n_samples;    /* M >= 1 samples per frame */
+    const double *coords; /* HOST, (T*M, 2) */
+    const void *sens;     /* DEVICE complex64 (C, nx, ny); copied */
+    int32_t device;       /* CUDA ordinal */
+    int32_t reserved;
+} csr_plan_desc;
+
+typedef struct csr_plan_info {
+    int64_t factor_bytes;    /* resident encoding factors */
+    int64_t workspace_bytes; /* scratch owned by the plan */
+    int32_t gemm_path;       /* 1 = tcgen05 tensor-core GEMMs, 0 = SIMT */
+    int32_t split_k;         /* adjoint split-K factor */
+} csr_plan_info;
+
+int csr_plan_create(const csr_plan_desc *desc, csr_plan **out);
+int csr_plan_destroy(csr_plan *plan);
+int csr_plan_get_info(const csr_plan *plan, csr_plan_info *info);
+
+/* Copy frame t's factors P0 (M, nx) and P1 (M, ny) (complex64) out —
+ * build_factors / DftFactors (operators.py:30-82). */
+int csr_plan_get_factors(const csr_plan *plan, int32_t frame, void *p0,
+                         void *p1, void *stream);
+
+/* DftOperator.forward (operators.py:185-193 -> kernels.nudft_forward_sep,
+ * kernels.py:71-78): image (T, nx, ny) -> kdata (T*M, C). */
+int csr_forward(csr_plan *plan, const void *image, void *kdata, void *stream);
+
+/* DftOperator.adjoint (operators.py:195-203 -> kernels.nudft_adjoint_sep,
+ * kernels.py:81-88): kdata (T*M, C) -> image (T, nx, ny); no 1/N. */
+int csr_adjoint(csr_plan *plan, const void *kdata, void *image, void *stream);
+
+/* normal_operator (solver.py:128-139) without the allreduce:
+ * out = F^H F x + (beta/2) Theta^H Theta x. */
+int csr_normal(csr_plan *plan, const void *x, void *out, double beta,
+               void *stream);
+
+/* transform.theta (transform.py:14-18 -> kernels.py:91-95): img (T,nx,ny)
+ * -> diffs (D, T, nx, ny), D = 2 for T == 1 (the reference) and 3 for T > 1
+ * (temporal component, extension). */
+int csr_theta(int32_t n_frames, int32_t nx, int32_t ny, const void *img,
+              void *diffs, void *stream);
+/* transform.theta_adjoint (transform.py:21-26 -> kernels.py:98-101). */
+int csr_theta_adjoint(int32_t n_frames, int32_t nx, int32_t ny,
+                      const void *diffs, void *img, void *stream);
+/* transform.soft_threshold (transform.py:29-42 -> kernels.py:104-108):
+ * z*(1 - t/|z|) where |z| > t else 0; t < 0 -> CSR_ERR_ARG. */
+int csr_soft_threshold(const void *z, int64_t n, float threshold, void *out,
+                       void *stream);
+/* tensor.hermitian_dot (tensor.py:44-50): out = sum conj(a)*b accumulated
+ * in f64; out is DEVICE double[2] (re, im).  Deterministic. */
+int csr_hermitian_dot(const void *a, const void *b, int64_t n, double *out,
+                      void *stream);
+/* sum |z| over complex64 z in f64 (objective's l1 term, solver.py:204);
+ * out is DEVICE double[1]. */
+int csr_abs_sum(const void *z, int64_t n, double *out, void *stream);
+/* tensor.axpy (tensor.py:58-64): out = y + alpha*x, alpha cast to
+ * complex64 first.  out may alias y. */
+int csr_axpy(double alpha_re, double alpha_im, const void *x, const void *y,
+             int64_t n, void *out, void *stream);
+
+/* ReconParams (solver.py:34-61) + lam_t for the temporal term. */
+typedef struct csr_admm_params {
+    double lam, lam_t, beta, admm_rtol, cg_atol;
+    int32_t admm_max_iters, cg_max_iters;
+} csr_admm_params;
+
+/* One RunReport.iterations record (solver.py:316-324). */
+typedef struct csr_iter_log {
+    int32_t iteration, cg_iterations;
+    double alpha, cg_final_residual_sq;
+} csr_iter_log;
+
+typedef struct csr_run_stats {
+    int32_t n_iterations;     /* ADMM iterations executed */
+    int32_t allreduce_calls;  /* image collectives issued (CommStats) */
+    double setup_ms, solve_ms; /* device time: F^H d setup, ADMM loop */
+    int32_t graph_used;       /* 1 if the iteration ran as a CUDA graph */
+    int32_t kernels_per_iter; /* kernel launches per ADMM iteration */
+} csr_run_stats;
+
+/* admm_reconstruct (solver.py:274-360) on this plan's device: rho0 = fhd =
+ * allreduce(F^H d) (two setup collectives, solver.py:307-309), then the ADMM
+ * loop (admm_step, solver.py:163-194) with zero-start CG (cg_solve,
+ * solver.py:87-125) and one image allreduce per CG iteration when a comm
+ * is attached.  kdata (T*M, C) device; rho_out (T, nx, ny) device;
+ * log = HOST array of admm_max_iters records.  Non-finite CG residual ->
+ * CSR_ERR_NONFINITE (CgDivergenceError).  snapshots (device, optional):
+ * (admm_max_iters+1, T, nx, ny) receives rho0 and the image after every
+ * iteration (the reference's rank-0 snapshots, solver.py:315-324). */
+int csr_admm_run(csr_plan *plan, const csr_admm_params *params,
+                 const void *kdata, void *rho_out, csr_iter_log *log,
+                 csr_run_stats *stats, void *stream, void *snapshots);
+
+/* Benchmark timing for csr_admm_run on this plan: when iter_ms (HOST,
+ * >= admm_max_iters floats) is set, every ADMM iteration is bracketed by
+ * CUDA events on the plan stream and its device time written there; when
+ * flush_buf (DEVICE, flush_bytes > L2) is also set, a buffer-overwrite
+ * kernel evicts L2 between iterations, outside the timed intervals.
+ * solve_ms then is the sum of the per-iteration times.  NULLs disable. */
+int csr_plan_set_timing(csr_plan *plan, void *flush_buf, int64_t flush_bytes,
+                        float *iter_ms);
+
+/* adjoint_reconstruct (solver.py:363-406): image = allreduce(F^H d). */
+int csr_adjoint_reconstruct(csr_plan *plan, const void *kdata, void *image,
+                            void *stream);
+
+/* NCCL communicator for coil-sharded runs (replaces the thread-barrier
+ * allreduce of sharding._Collective, sharding.py:211-250).  Rank 0 makes
+ * the 128-byte unique id, the host broadcasts it (torch.distributed), every
+ * rank creates its comm on its own device and attaches it to its plan. */
+int csr_comm_unique_id(void *id128);
+int csr_comm_create(const void *id128, int32_t nranks, int32_t rank,
+                    int32_t device, csr_comm **out);
+int csr_comm_destroy(csr_comm *comm);
+int csr_plan_set_comm(csr_plan *plan, csr_comm *comm);
+/* In-place sum allreduce of n floats (device) over the comm. */
+int csr_comm_allreduce(csr_comm *comm, void *buf, int64_t n_floats,
+                       void *stream);
+
+const char *csr_last_error(void);
+/* Number of this library's kernels launched since load (diagnostics). */
+int64_t csr_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSRECON_B200_H */

@@ -1,0 +1,96 @@
+// Shared helpers for the csrecon_b200 kernels: complex64 arithmetic,
+// deterministic two-stage reductions, launch bookkeeping.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace csr {
+
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+__host__ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+    return make_float2(a.x + b.x, a.y + b.y);
+}
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
+    return make_float2(a.x - b.x, a.y - b.y);
+}
+__host__ __device__ __forceinline__ float2 cconj(float2 a) {
+    return make_float2(a.x, -a.y);
+}
+// acc += a * b
+__device__ __forceinline__ void cfma(float2 &acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x);
+    acc.x = fmaf(-a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, b.y, acc.y);
+    acc.y = fmaf(a.y, b.x, acc.y);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic grid reduction of NV doubles: every block writes its
+// partial, the last block to arrive (ticket) folds the partials in block
+// order and returns true with the totals in `tot` (valid in thread 0).
+// Requires blockDim.x to be a multiple of 32 and <= 1024.
+template <int NV>
+__device__ bool grid_reduce(double (&v)[NV], double *partials,
+                            unsigned *ticket, double (&tot)[NV]) {
+    __shared__ double sh[NV][32];
+    __shared__ int last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double w = warp_sum(v[i]);
+        if (lane == 0) sh[i][warp] = w;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double w = lane < nwarps ? sh[i][lane] : 0.0;
+            w = warp_sum(w);
+            if (lane == 0) partials[(size_t)blockIdx.x * NV + i] = w;
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double w = 0.0;
+            for (unsigned b = lane; b < gridDim.x; b += 32)
+                w += __ldcg(partials + (size_t)b * NV + i);
+            w = warp_sum(w);
+            tot[i] = w;
+        }
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+    return true;
+}
+
+// Grid size used by every reduction kernel over n elements: a function of n
+// only, so reductions are run-to-run deterministic.
+inline int reduce_blocks(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b > 4 * 148) b = 4 * 148;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+}  // namespace csr

@@ -1,0 +1,731 @@
+// csrecon_b200: C-ABI implementation (plan, operators, native ADMM loop).
+// See include/csrecon_b200.h for the contract and the reference interfaces
+// each entry point replaces.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/csrecon_b200.h"
+#include "common.cuh"
+#include "elementwise.cuh"
+#include "nudft_simt.cuh"
+#include "nudft_tc.cuh"
+
+using namespace csr;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                             \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess)                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? CSR_ERR_OOM        \
+                                                        : CSR_ERR_CUDA,      \
+                        std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NC(call)                                                          \
+    do {                                                                  \
+        ncclResult_t r_ = (call);                                         \
+        if (r_ != ncclSuccess)                                            \
+            return fail(CSR_ERR_NCCL,                                     \
+                        std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+#define LAUNCHED()                                              \
+    do {                                                        \
+        g_launches.fetch_add(1, std::memory_order_relaxed);     \
+        cudaError_t e_ = cudaGetLastError();                    \
+        if (e_ != cudaSuccess)                                  \
+            return fail(CSR_ERR_CUDA, std::string("kernel launch: ") + \
+                                          cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int TPB = 256;
+
+inline int ew_blocks(int64_t n) { return reduce_blocks(n, TPB); }
+
+}  // namespace
+
+struct csr_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0, device = 0;
+};
+
+struct csr_plan {
+    int dev = 0;
+    int T = 1, nx = 0, ny = 0, C = 0;
+    int64_t M = 0;
+    Geom g{};
+    float2 *P0 = nullptr, *P1 = nullptr, *sens = nullptr;
+    float2 *kd = nullptr, *ws = nullptr, *fhf = nullptr;
+    int S = 1, kchunk = 0;
+    // tensor-core operands (nudft_tc.cuh); tc.enabled == false -> SIMT
+    TcPlan tc;
+    // ADMM state
+    float2 *rho[2] = {nullptr, nullptr}, *mu = nullptr, *eta = nullptr,
+           *fhd = nullptr, *r = nullptr, *d = nullptr, *ad = nullptr;
+    double *partials = nullptr;
+    unsigned *tickets = nullptr;
+    DevScalars *sc = nullptr;
+    IterLog *log = nullptr;
+    int log_cap = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {};
+    cudaGraphExec_t graph = nullptr;
+    std::vector<double> graph_key;
+    int kernels_per_iter = 0;
+    csr_comm *comm = nullptr;
+    int64_t factor_bytes = 0, ws_bytes = 0;
+    // benchmark timing (csr_plan_set_timing)
+    void *flush_buf = nullptr;
+    int64_t flush_bytes = 0;
+    float *iter_ms = nullptr;
+    std::vector<cudaEvent_t> iter_ev;
+    std::vector<void *> allocs;
+};
+
+namespace {
+
+template <class T>
+int dalloc(csr_plan *p, T **ptr, size_t count, int64_t *acct) {
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    void *v = nullptr;
+    cudaError_t e = cudaMalloc(&v, bytes);
+    if (e != cudaSuccess)
+        return fail(CSR_ERR_OOM, std::string("cudaMalloc(") + std::to_string(bytes) +
+                                     "): " + cudaGetErrorString(e));
+    p->allocs.push_back(v);
+    *ptr = static_cast<T *>(v);
+    if (acct) *acct += (int64_t)bytes;
+    return CSR_OK;
+}
+
+#define TRY(x)                  \
+    do {                        \
+        int rc_ = (x);          \
+        if (rc_ != CSR_OK) return rc_; \
+    } while (0)
+
+int check_device(int dev) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(CSR_ERR_CUDA, "no CUDA device available (csrecon_b200 has no CPU fallback)");
+    if (dev < 0 || dev >= n) return fail(CSR_ERR_ARG, "device ordinal out of range");
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        return fail(CSR_ERR_CUDA, std::string("csrecon_b200 is built for sm_100a; device is ") +
+                                      prop.name);
+    return CSR_OK;
+}
+
+// F x on the plan (x: (T,nx,ny) -> out (T*M, C))
+int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
+                const int *gate) {
+    if (p->tc.enabled) {
+        TRY(tc_forward(p->tc, x, p->sens, out, st, gate));
+        g_launches.fetch_add(p->tc.fwd_launches, std::memory_order_relaxed);
+        return CSR_OK;
+    }
+    dim3 grid((unsigned)((p->M + ST - 1) / ST), (unsigned)p->C, (unsigned)p->T);
+    k_forward_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, p->sens, x, out, (int)p->M,
+                                         p->nx, p->ny, p->C, gate);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+// split-K adjoint partials into p->ws (then coil-combined by a reduce kernel)
+int run_adjoint_partials(csr_plan *p, const float2 *kd, cudaStream_t st,
+                         const int *gate) {
+    if (p->tc.enabled) {
+        TRY(tc_adjoint(p->tc, kd, p->ws, st, gate));
+        g_launches.fetch_add(p->tc.adj_launches, std::memory_order_relaxed);
+        return CSR_OK;
+    }
+    int tiles = ((p->nx + ST - 1) / ST) * ((p->ny + ST - 1) / ST);
+    dim3 grid((unsigned)tiles, (unsigned)p->C, (unsigned)(p->T * p->S));
+    k_adjoint_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, kd, p->ws, (int)p->M, p->nx,
+                                         p->ny, p->C, p->T, p->kchunk, gate);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int run_adjoint(csr_plan *p, const float2 *kd, float2 *img, cudaStream_t st) {
+    TRY(run_adjoint_partials(p, kd, st, nullptr));
+    k_adj_reduce<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->S, p->C, p->ws, p->sens,
+                                                    img, nullptr);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int allreduce(csr_plan *p, float2 *buf, int64_t n_complex, cudaStream_t st) {
+    if (!p->comm || p->comm->nranks == 1) return CSR_OK;
+    NC(ncclAllReduce(buf, buf, (size_t)(2 * n_complex), ncclFloat, ncclSum,
+                     p->comm->comm, st));
+    return CSR_OK;
+}
+
+AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
+    AdmmBufs b;
+    b.rho[0] = p->rho[0];
+    b.rho[1] = p->rho[1];
+    b.mu = p->mu;
+    b.eta = p->eta;
+    b.fhd = p->fhd;
+    b.r = p->r;
+    b.d = p->d;
+    b.ad = p->ad;
+    b.fhf = p->fhf;
+    b.partials = p->partials;
+    b.tickets = p->tickets;
+    b.s = p->sc;
+    b.log = p->log;
+    // scalars cast to the working precision as the reference does
+    // (transform.py:39-41: the threshold is cast to the real dtype)
+    b.t_s = (float)(prm->lam / prm->beta);
+    double lt = prm->lam_t > 0 ? prm->lam_t : prm->lam;
+    b.t_t = (float)(lt / prm->beta);
+    b.hb = (float)(prm->beta / 2);
+    return b;
+}
+
+// One ADMM iteration as a fixed kernel sequence (captured as a graph).
+int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
+                           cudaStream_t st, int *nk) {
+    const Geom g = p->g;
+    const int eb = ew_blocks(g.n), ebD = ew_blocks(g.n * g.D);
+    int k = 0;
+    k_admm_mu<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    k_admm_rhs<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    const int *gate = &p->sc->cg_active;
+    const bool multi = p->comm && p->comm->nranks > 1;
+    for (int it = 0; it < cg_max; ++it) {
+        TRY(run_forward(p, p->d, p->kd, st, gate));
+        k += p->tc.enabled ? p->tc.fwd_launches : 1;
+        TRY(run_adjoint_partials(p, p->kd, st, gate));
+        k += p->tc.enabled ? p->tc.adj_launches : 1;
+        if (multi) {
+            k_cg_fhf<<<eb, TPB, 0, st>>>(g, b, p->ws, p->sens, p->S, p->C); LAUNCHED(); ++k;
+            TRY(allreduce(p, p->fhf, g.n, st));
+            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, nullptr, p->sens, p->S, p->C); LAUNCHED(); ++k;
+        } else {
+            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, p->ws, p->sens, p->S, p->C); LAUNCHED(); ++k;
+        }
+        k_cg_xr<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+        k_cg_d<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    }
+    k_admm_post<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    k_snapshot<<<eb, TPB, 0, st>>>(g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
+    *nk = k;
+    return CSR_OK;
+}
+
+__global__ void k_flush(uint4 *buf, int64_t n, unsigned v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = make_uint4(v, v, v, v);
+}
+
+__global__ void k_copy_cur(int64_t n, const DevScalars *s, const float2 *r0,
+                           const float2 *r1, float2 *out) {
+    const float2 *src = s->cur ? r1 : r0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = src[i];
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char *csr_last_error(void) { return g_err.c_str(); }
+int64_t csr_kernel_launches(void) { return g_launches.load(); }
+
+int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
+    if (!desc || !out) return fail(CSR_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (desc->nx < 1 || desc->ny < 1 || desc->n_frames < 1 || desc->n_coils < 1 ||
+        desc->n_samples < 1)
+        return fail(CSR_ERR_SHAPE, "plan dimensions must all be >= 1");
+    if (!desc->coords || !desc->sens) return fail(CSR_ERR_ARG, "coords and sens are required");
+    TRY(check_device(desc->device));
+    CU(cudaSetDevice(desc->device));
+    csr_plan *p = new csr_plan();
+    p->dev = desc->device;
+    p->T = desc->n_frames;
+    p->nx = desc->nx;
+    p->ny = desc->ny;
+    p->C = desc->n_coils;
+    p->M = desc->n_samples;
+    p->g = make_geom(p->T, p->nx, p->ny);
+    const int64_t rows = (int64_t)p->T * p->M;
+    const int64_t nxy = (int64_t)p->nx * p->ny;
+    auto cleanup = [&](int rc) {
+        csr_plan_destroy(p);
+        return rc;
+    };
+    int rc;
+    if ((rc = dalloc(p, &p->P0, (size_t)(rows * p->nx), &p->factor_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->P1, (size_t)(rows * p->ny), &p->factor_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->sens, (size_t)(p->C * nxy), &p->factor_bytes))) return cleanup(rc);
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(CSR_ERR_CUDA, "stream create failed"));
+    p->stream = st;
+    for (auto &e : p->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "event create"));
+    // coords -> device, factors in f64 -> complex64
+    double *dcoords = nullptr;
+    if (cudaMalloc(&dcoords, rows * 2 * sizeof(double)) != cudaSuccess)
+        return cleanup(fail(CSR_ERR_OOM, "coords alloc"));
+    p->allocs.push_back(dcoords);
+    if (cudaMemcpyAsync(dcoords, desc->coords, rows * 2 * sizeof(double),
+                        cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(p->sens, desc->sens, p->C * nxy * sizeof(float2),
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return cleanup(fail(CSR_ERR_CUDA, "plan upload failed"));
+    {
+        int64_t total = rows * (p->nx + p->ny);
+        int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+        k_factors<<<blocks, 256, 0, st>>>(dcoords, rows, p->nx, p->ny, p->P0, p->P1);
+        g_launches.fetch_add(1);
+        if (cudaGetLastError() != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "k_factors launch"));
+    }
+    // tensor-core operand build (returns tc.enabled=false for shapes it
+    // does not tile; the SIMT kernels then handle the plan)
+    if ((rc = tc_plan_build(p->tc, p->T, p->nx, p->ny, p->C, p->M, p->P0, p->P1, st,
+                            &p->factor_bytes, &p->ws_bytes, p->allocs)))
+        return cleanup(fail(rc, "tensor-core plan: " + g_err));
+    // workspace
+    if ((rc = dalloc(p, &p->kd, (size_t)(rows * p->C), &p->ws_bytes))) return cleanup(rc);
+    if (p->tc.enabled) {
+        p->S = p->tc.split;
+        p->ws = p->tc.ws;
+    } else {
+        int tiles = ((p->nx + ST - 1) / ST) * ((p->ny + ST - 1) / ST);
+        int64_t blocks = (int64_t)tiles * p->C * p->T;
+        int64_t S = (4 * 148 + blocks - 1) / blocks;
+        int64_t smax = (p->M + 255) / 256;
+        if (S > smax) S = smax;
+        if (S < 1) S = 1;
+        int64_t kc = (p->M + S - 1) / S;
+        kc = (kc + SK - 1) / SK * SK;
+        S = (p->M + kc - 1) / kc;
+        p->S = (int)S;
+        p->kchunk = (int)kc;
+        if ((rc = dalloc(p, &p->ws, (size_t)(S * p->T * p->C * nxy), &p->ws_bytes)))
+            return cleanup(rc);
+    }
+    const int64_t n = p->g.n, nD = n * p->g.D;
+    if ((rc = dalloc(p, &p->fhf, (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    for (int i = 0; i < 2; ++i)
+        if ((rc = dalloc(p, &p->rho[i], (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->mu, (size_t)nD, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->eta, (size_t)nD, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->fhd, (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->r, (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->d, (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->ad, (size_t)n, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->partials, (size_t)(4 * 148 * 4), &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->tickets, 8, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->sc, 1, &p->ws_bytes))) return cleanup(rc);
+    if (cudaMemsetAsync(p->tickets, 0, 8 * sizeof(unsigned), st) != cudaSuccess)
+        return cleanup(fail(CSR_ERR_CUDA, "memset"));
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return cleanup(fail(CSR_ERR_CUDA, std::string("plan build: ") +
+                                              cudaGetErrorString(cudaGetLastError())));
+    *out = p;
+    return CSR_OK;
+}
+
+int csr_plan_destroy(csr_plan *p) {
+    if (!p) return CSR_OK;
+    cudaSetDevice(p->dev);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    for (void *a : p->allocs) cudaFree(a);
+    if (p->log) cudaFree(p->log);
+    for (auto &e : p->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : p->iter_ev) cudaEventDestroy(e);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+    return CSR_OK;
+}
+
+int csr_plan_get_info(const csr_plan *p, csr_plan_info *info) {
+    if (!p || !info) return fail(CSR_ERR_ARG, "null argument");
+    info->factor_bytes = p->factor_bytes;
+    info->workspace_bytes = p->ws_bytes;
+    info->gemm_path = p->tc.enabled ? 1 : 0;
+    info->split_k = p->S;
+    return CSR_OK;
+}
+
+int csr_plan_get_factors(const csr_plan *p, int32_t frame, void *p0, void *p1,
+                         void *stream) {
+    if (!p || frame < 0 || frame >= p->T) return fail(CSR_ERR_ARG, "bad frame");
+    CU(cudaSetDevice(p->dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(p0, p->P0 + (int64_t)frame * p->M * p->nx,
+                       p->M * p->nx * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(p1, p->P1 + (int64_t)frame * p->M * p->ny,
+                       p->M * p->ny * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    return CSR_OK;
+}
+
+int csr_forward(csr_plan *p, const void *image, void *kdata, void *stream) {
+    if (!p || !image || !kdata) return fail(CSR_ERR_ARG, "null argument");
+    CU(cudaSetDevice(p->dev));
+    return run_forward(p, (const float2 *)image, (float2 *)kdata, (cudaStream_t)stream, nullptr);
+}
+
+int csr_adjoint(csr_plan *p, const void *kdata, void *image, void *stream) {
+    if (!p || !image || !kdata) return fail(CSR_ERR_ARG, "null argument");
+    CU(cudaSetDevice(p->dev));
+    return run_adjoint(p, (const float2 *)kdata, (float2 *)image, (cudaStream_t)stream);
+}
+
+int csr_normal(csr_plan *p, const void *x, void *out, double beta, void *stream) {
+    if (!p || !x || !out) return fail(CSR_ERR_ARG, "null argument");
+    CU(cudaSetDevice(p->dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    TRY(run_forward(p, (const float2 *)x, p->kd, st, nullptr));
+    TRY(run_adjoint(p, p->kd, p->fhf, st));
+    k_normal_finish<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->fhf, (const float2 *)x,
+                                                       (float)(beta / 2), (float2 *)out);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int csr_theta(int32_t T, int32_t nx, int32_t ny, const void *img, void *diffs,
+              void *stream) {
+    if (T < 1 || nx < 1 || ny < 1) return fail(CSR_ERR_SHAPE, "bad geometry");
+    Geom g = make_geom(T, nx, ny);
+    k_theta<<<ew_blocks(g.n * g.D), TPB, 0, (cudaStream_t)stream>>>(
+        g, (const float2 *)img, (float2 *)diffs);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int csr_theta_adjoint(int32_t T, int32_t nx, int32_t ny, const void *diffs,
+                      void *img, void *stream) {
+    if (T < 1 || nx < 1 || ny < 1) return fail(CSR_ERR_SHAPE, "bad geometry");
+    Geom g = make_geom(T, nx, ny);
+    k_theta_adj<<<ew_blocks(g.n), TPB, 0, (cudaStream_t)stream>>>(
+        g, (const float2 *)diffs, (float2 *)img);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int csr_soft_threshold(const void *z, int64_t n, float t, void *out, void *stream) {
+    if (!(t >= 0.f)) return fail(CSR_ERR_ARG, "threshold must be >= 0");
+    if (n <= 0) return CSR_OK;
+    k_soft<<<ew_blocks(n), TPB, 0, (cudaStream_t)stream>>>((const float2 *)z, n, t,
+                                                           (float2 *)out);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int csr_hermitian_dot(const void *a, const void *b, int64_t n, double *out,
+                      void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        CU(cudaMemsetAsync(out, 0, 2 * sizeof(double), st));
+        return CSR_OK;
+    }
+    int blocks = ew_blocks(n);
+    void *scratch = nullptr;
+    size_t bytes = (size_t)blocks * 2 * sizeof(double) + 16;
+    CU(cudaMallocAsync(&scratch, bytes, st));
+    unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * 2 * sizeof(double));
+    CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
+    k_hdot<<<blocks, TPB, 0, st>>>((const float2 *)a, (const float2 *)b, n,
+                                   (double *)scratch, ticket, out);
+    LAUNCHED();
+    CU(cudaFreeAsync(scratch, st));
+    return CSR_OK;
+}
+
+int csr_abs_sum(const void *z, int64_t n, double *out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        CU(cudaMemsetAsync(out, 0, sizeof(double), st));
+        return CSR_OK;
+    }
+    int blocks = ew_blocks(n);
+    void *scratch = nullptr;
+    CU(cudaMallocAsync(&scratch, (size_t)blocks * sizeof(double) + 16, st));
+    unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * sizeof(double));
+    CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
+    k_abs_sum<<<blocks, TPB, 0, st>>>((const float2 *)z, n, (double *)scratch, ticket, out);
+    LAUNCHED();
+    CU(cudaFreeAsync(scratch, st));
+    return CSR_OK;
+}
+
+int csr_axpy(double are, double aim, const void *x, const void *y, int64_t n,
+             void *out, void *stream) {
+    if (n <= 0) return CSR_OK;
+    k_axpy<<<ew_blocks(n), TPB, 0, (cudaStream_t)stream>>>(
+        make_float2((float)are, (float)aim), (const float2 *)x, (const float2 *)y, n,
+        (float2 *)out);
+    LAUNCHED();
+    return CSR_OK;
+}
+
+int csr_adjoint_reconstruct(csr_plan *p, const void *kdata, void *image, void *stream) {
+    if (!p || !kdata || !image) return fail(CSR_ERR_ARG, "null argument");
+    CU(cudaSetDevice(p->dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    TRY(run_adjoint(p, (const float2 *)kdata, (float2 *)image, st));
+    TRY(allreduce(p, (float2 *)image, p->g.n, st));
+    return CSR_OK;
+}
+
+int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
+                 void *rho_out, csr_iter_log *log, csr_run_stats *stats,
+                 void *stream, void *snapshots) {
+    if (!p || !prm || !kdata || !rho_out || !log) return fail(CSR_ERR_ARG, "null argument");
+    if (!(prm->lam > 0) || !(prm->beta > 0))
+        return fail(CSR_ERR_ARG, "lam and beta must be > 0");
+    if (!(prm->admm_rtol > 0) || !(prm->cg_atol > 0))
+        return fail(CSR_ERR_ARG, "admm_rtol and cg_atol must be > 0");
+    if (prm->admm_max_iters < 1 || prm->cg_max_iters < 1)
+        return fail(CSR_ERR_ARG, "iteration caps must be >= 1");
+    CU(cudaSetDevice(p->dev));
+    cudaStream_t caller = (cudaStream_t)stream;
+    cudaStream_t st = p->stream;
+    const Geom g = p->g;
+    const int64_t n = g.n, nD = g.n * g.D;
+    if (p->log_cap < prm->admm_max_iters) {
+        if (p->log) cudaFree(p->log);
+        p->log = nullptr;
+        CU(cudaMalloc(&p->log, sizeof(IterLog) * prm->admm_max_iters));
+        p->log_cap = prm->admm_max_iters;
+        if (p->graph) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+    }
+    CU(cudaEventRecord(p->ev[0], caller));
+    CU(cudaStreamWaitEvent(st, p->ev[0], 0));
+    int ar_calls = 0;
+    // ---- setup: rho0 = fhd = allreduce(F^H d)  (solver.py:306-309)
+    CU(cudaEventRecord(p->ev[0], st));
+    TRY(run_adjoint(p, (const float2 *)kdata, p->fhd, st));
+    CU(cudaMemcpyAsync(p->rho[0], p->fhd, n * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    if (p->comm && p->comm->nranks > 1) {
+        TRY(allreduce(p, p->rho[0], n, st));
+        TRY(allreduce(p, p->fhd, n, st));
+        ar_calls += 2;
+    }
+    CU(cudaMemsetAsync(p->mu, 0, nD * sizeof(float2), st));
+    CU(cudaMemsetAsync(p->eta, 0, nD * sizeof(float2), st));
+    DevScalars h{};
+    h.atol2 = prm->cg_atol * prm->cg_atol;
+    h.rtol2 = prm->admm_rtol * prm->admm_rtol;
+    h.cg_max = prm->cg_max_iters;
+    h.admm_max = prm->admm_max_iters;
+    h.admm_alpha = 1.0;
+    h.admm_active = (1.0 > h.rtol2) ? 1 : 0;  // should_continue(0, 1.0)
+    h.snap = (float2 *)snapshots;
+    if (snapshots)
+        CU(cudaMemcpyAsync(snapshots, p->rho[0], n * sizeof(float2),
+                           cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(p->sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(p->ev[1], st));
+    // ---- ADMM loop as a CUDA graph of one iteration
+    AdmmBufs b = admm_bufs(p, prm);
+    std::vector<double> key = {prm->lam, prm->lam_t, prm->beta,
+                               (double)prm->cg_max_iters,
+                               (double)(p->comm ? p->comm->nranks : 1)};
+    bool use_graph = true;
+    if (!p->graph || p->graph_key != key) {
+        if (p->graph) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        cudaGraph_t graph = nullptr;
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int nk = 0;
+        int rc = enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk);
+        cudaError_t ec = cudaStreamEndCapture(st, &graph);
+        if (rc != CSR_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        if (ec != cudaSuccess || !graph) {
+            use_graph = false;
+            cudaGetLastError();
+        } else {
+            cudaError_t ei = cudaGraphInstantiate(&p->graph, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ei != cudaSuccess) {
+                use_graph = false;
+                p->graph = nullptr;
+                cudaGetLastError();
+            }
+        }
+        p->kernels_per_iter = nk;
+        p->graph_key = key;
+    }
+    const bool timed = p->iter_ms != nullptr;
+    if (timed) {
+        while ((int)p->iter_ev.size() < 2 * prm->admm_max_iters) {
+            cudaEvent_t e;
+            CU(cudaEventCreate(&e));
+            p->iter_ev.push_back(e);
+        }
+    }
+    for (int it = 0; it < prm->admm_max_iters; ++it) {
+        if (timed && p->flush_buf) {
+            int64_t n16 = p->flush_bytes / 16;
+            k_flush<<<148 * 8, 512, 0, st>>>((uint4 *)p->flush_buf, n16, (unsigned)it);
+            LAUNCHED();
+        }
+        if (timed) CU(cudaEventRecord(p->iter_ev[2 * it], st));
+        if (use_graph) {
+            CU(cudaGraphLaunch(p->graph, st));
+        } else {
+            int nk = 0;
+            TRY(enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk));
+        }
+        if (timed) CU(cudaEventRecord(p->iter_ev[2 * it + 1], st));
+    }
+    CU(cudaEventRecord(p->ev[2], st));
+    k_copy_cur<<<ew_blocks(n), TPB, 0, st>>>(n, p->sc, p->rho[0], p->rho[1], (float2 *)rho_out);
+    LAUNCHED();
+    CU(cudaEventRecord(p->ev[3], st));
+    CU(cudaStreamWaitEvent(caller, p->ev[3], 0));
+    // ---- host-side report
+    DevScalars hs{};
+    std::vector<IterLog> hl(prm->admm_max_iters);
+    CU(cudaMemcpyAsync(&hs, p->sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hl.data(), p->log, sizeof(IterLog) * prm->admm_max_iters,
+                       cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int i = 0; i < hs.admm_iter; ++i) {
+        log[i].iteration = hl[i].iteration;
+        log[i].cg_iterations = hl[i].cg_iterations;
+        log[i].alpha = hl[i].alpha;
+        log[i].cg_final_residual_sq = hl[i].cg_final_residual_sq;
+    }
+    if (stats) {
+        float ms_setup = 0.f, ms_solve = 0.f;
+        cudaEventElapsedTime(&ms_setup, p->ev[0], p->ev[1]);
+        cudaEventElapsedTime(&ms_solve, p->ev[1], p->ev[2]);
+        stats->n_iterations = hs.admm_iter;
+        int cg_total = 0;
+        for (int i = 0; i < hs.admm_iter; ++i) cg_total += hl[i].cg_iterations;
+        if (hs.error) cg_total += hs.cg_iter;
+        stats->allreduce_calls = ar_calls + ((p->comm && p->comm->nranks > 1) ? cg_total : 0);
+        stats->setup_ms = ms_setup;
+        stats->solve_ms = ms_solve;
+        if (timed) {
+            double tot = 0.0;
+            for (int it = 0; it < prm->admm_max_iters; ++it) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, p->iter_ev[2 * it], p->iter_ev[2 * it + 1]);
+                p->iter_ms[it] = ms;
+                tot += ms;
+            }
+            stats->solve_ms = tot;
+        }
+        stats->graph_used = use_graph ? 1 : 0;
+        stats->kernels_per_iter = p->kernels_per_iter;
+    }
+    if (hs.error)
+        return fail(CSR_ERR_NONFINITE, "residual became non-finite at CG step " +
+                                           std::to_string(hs.cg_iter) + " of ADMM iteration " +
+                                           std::to_string(hs.admm_iter + 1));
+    return CSR_OK;
+}
+
+// ---- NCCL ---------------------------------------------------------------
+int csr_plan_set_timing(csr_plan *p, void *flush_buf, int64_t flush_bytes,
+                        float *iter_ms) {
+    if (!p) return fail(CSR_ERR_ARG, "null plan");
+    p->flush_buf = flush_buf;
+    p->flush_bytes = flush_buf ? flush_bytes : 0;
+    p->iter_ms = iter_ms;
+    return CSR_OK;
+}
+
+int csr_comm_unique_id(void *id128) {
+    if (!id128) return fail(CSR_ERR_ARG, "null argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+    return CSR_OK;
+}
+
+int csr_comm_create(const void *id128, int32_t nranks, int32_t rank, int32_t device,
+                    csr_comm **out) {
+    if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(CSR_ERR_ARG, "bad communicator arguments");
+    TRY(check_device(device));
+    CU(cudaSetDevice(device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    csr_comm *c = new csr_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(CSR_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+    return CSR_OK;
+}
+
+int csr_comm_destroy(csr_comm *c) {
+    if (!c) return CSR_OK;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+    return CSR_OK;
+}
+
+int csr_plan_set_comm(csr_plan *p, csr_comm *c) {
+    if (!p) return fail(CSR_ERR_ARG, "null plan");
+    if (c && c->device != p->dev) return fail(CSR_ERR_ARG, "comm and plan on different devices");
+    p->comm = c;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return CSR_OK;
+}
+
+int csr_comm_allreduce(csr_comm *c, void *buf, int64_t n_floats, void *stream) {
+    if (!c) return fail(CSR_ERR_ARG, "null comm");
+    if (c->nranks == 1) return CSR_OK;
+    CU(cudaSetDevice(c->device));
+    NC(ncclAllReduce(buf, buf, (size_t)n_floats, ncclFloat, ncclSum, c->comm,
+                     (cudaStream_t)stream));
+    return CSR_OK;
+}
+
+}  // extern "C"

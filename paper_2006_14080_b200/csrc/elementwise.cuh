@@ -1,0 +1,464 @@
+// Bandwidth-bound kernels: encoding factors (K10), finite differences and
+// their adjoint (K5/K6), soft threshold (K7), dots (K8), axpy (K9), and the
+// fused CG / ADMM update kernels of the native solver loop.
+//
+// Image layout (T, nx, ny) complex64, pixel p = (t*nx + x)*ny + y; theta
+// stacks (D, T, nx, ny) with D = 2 (static, kernels.py:91-101) or 3 (2-D+t:
+// third component along t).  All kernels are grid-stride, 256 threads.
+#pragma once
+
+#include "common.cuh"
+
+namespace csr {
+
+struct Geom {
+    int T, nx, ny;
+    int64_t n;   // T*nx*ny
+    int D;       // theta components
+};
+
+__host__ __device__ inline Geom make_geom(int T, int nx, int ny) {
+    Geom g;
+    g.T = T; g.nx = nx; g.ny = ny;
+    g.n = (int64_t)T * nx * ny;
+    g.D = T > 1 ? 3 : 2;
+    return g;
+}
+
+// ---- K10: separable encoding factors, f64 angle, rounded once ----------
+// P0[t][k][x] = exp(-2 pi i kx rx), rx = x - nx//2 (operators.py:50-82,
+// acquisition.py:39-43).  The angle is (-2*pi) * (kx * rx) in f64, exactly
+// numpy's evaluation order; cos/sin in f64; one rounding to f32.
+__global__ void k_factors(const double *__restrict__ coords, int64_t rows,
+                          int nx, int ny, float2 *__restrict__ P0,
+                          float2 *__restrict__ P1) {
+    const double m2pi = -2.0 * 3.141592653589793;
+    int64_t total = rows * (int64_t)(nx + ny);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = i / (nx + ny);
+        int j = (int)(i - k * (nx + ny));
+        double kr;
+        float2 *dst;
+        if (j < nx) {
+            kr = coords[2 * k] * (double)(j - nx / 2);
+            dst = P0 + k * nx + j;
+        } else {
+            j -= nx;
+            kr = coords[2 * k + 1] * (double)(j - ny / 2);
+            dst = P1 + k * ny + j;
+        }
+        double ang = m2pi * kr;
+        double s, c;
+        sincos(ang, &s, &c);
+        *dst = make_float2((float)c, (float)s);
+    }
+}
+
+// ---- circular finite differences ----------------------------------------
+__device__ __forceinline__ float2 theta_at(const float2 *__restrict__ v,
+                                           const Geom &g, int comp, int t,
+                                           int x, int y) {
+    int64_t p = ((int64_t)t * g.nx + x) * g.ny + y;
+    int64_t q;
+    if (comp == 0) q = ((int64_t)t * g.nx + (x == 0 ? g.nx - 1 : x - 1)) * g.ny + y;
+    else if (comp == 1) q = ((int64_t)t * g.nx + x) * g.ny + (y == 0 ? g.ny - 1 : y - 1);
+    else q = ((int64_t)(t == 0 ? g.T - 1 : t - 1) * g.nx + x) * g.ny + y;
+    return csub(v[p], v[q]);
+}
+
+// theta^H applied to a stack given as a functor u(comp, t, x, y)
+template <class U>
+__device__ __forceinline__ float2 theta_adj_at(const U &u, const Geom &g, int t,
+                                               int x, int y) {
+    int xp = x + 1 == g.nx ? 0 : x + 1;
+    int yp = y + 1 == g.ny ? 0 : y + 1;
+    float2 r = cadd(csub(u(0, t, x, y), u(0, t, xp, y)),
+                    csub(u(1, t, x, y), u(1, t, x, yp)));
+    if (g.D == 3) {
+        int tp = t + 1 == g.T ? 0 : t + 1;
+        r = cadd(r, csub(u(2, t, x, y), u(2, tp, x, y)));
+    }
+    return r;
+}
+
+struct StackRef {
+    const float2 *s;
+    Geom g;
+    __device__ float2 operator()(int comp, int t, int x, int y) const {
+        return s[comp * g.n + ((int64_t)t * g.nx + x) * g.ny + y];
+    }
+};
+
+// Theta^H Theta x at one pixel, computed as theta then its adjoint
+// (the reference's composition, solver.py:139).
+struct ThetaOf {
+    const float2 *v;
+    Geom g;
+    __device__ float2 operator()(int comp, int t, int x, int y) const {
+        return theta_at(v, g, comp, t, x, y);
+    }
+};
+
+__device__ __forceinline__ void unflat(const Geom &g, int64_t p, int &t, int &x,
+                                       int &y) {
+    y = (int)(p % g.ny);
+    int64_t r = p / g.ny;
+    x = (int)(r % g.nx);
+    t = (int)(r / g.nx);
+}
+
+__global__ void k_theta(Geom g, const float2 *__restrict__ img,
+                        float2 *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int comp = (int)(i / g.n);
+        int t, x, y;
+        unflat(g, i - comp * g.n, t, x, y);
+        out[i] = theta_at(img, g, comp, t, x, y);
+    }
+}
+
+__global__ void k_theta_adj(Geom g, const float2 *__restrict__ stack,
+                            float2 *__restrict__ out) {
+    StackRef u{stack, g};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t, x, y;
+        unflat(g, i, t, x, y);
+        out[i] = theta_adj_at(u, g, t, x, y);
+    }
+}
+
+// kernels.py:201-209: out = z - z*(t/|z|) if |z| > t else 0
+__device__ __forceinline__ float2 soft1(float2 z, float t) {
+    float mag = hypotf(z.x, z.y);
+    if (mag > t) {
+        float s = t / mag;
+        return make_float2(z.x - z.x * s, z.y - z.y * s);
+    }
+    return make_float2(0.f, 0.f);
+}
+
+__global__ void k_soft(const float2 *__restrict__ z, int64_t n, float t,
+                       float2 *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = soft1(z[i], t);
+}
+
+// sum conj(a)*b in f64
+__global__ void k_hdot(const float2 *__restrict__ a, const float2 *__restrict__ b,
+                       int64_t n, double *partials, unsigned *ticket,
+                       double *out) {
+    double v[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 p = a[i], q = b[i];
+        v[0] += (double)p.x * q.x + (double)p.y * q.y;
+        v[1] += (double)p.x * q.y - (double)p.y * q.x;
+    }
+    double tot[2];
+    if (grid_reduce<2>(v, partials, ticket, tot) && threadIdx.x == 0) {
+        out[0] = tot[0];
+        out[1] = tot[1];
+    }
+}
+
+__global__ void k_abs_sum(const float2 *__restrict__ z, int64_t n,
+                          double *partials, unsigned *ticket, double *out) {
+    double v[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 p = z[i];
+        v[0] += (double)hypotf(p.x, p.y);
+    }
+    double tot[1];
+    if (grid_reduce<1>(v, partials, ticket, tot) && threadIdx.x == 0) out[0] = tot[0];
+}
+
+__global__ void k_axpy(float2 alpha, const float2 *__restrict__ x,
+                       const float2 *y, int64_t n, float2 *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = cadd(y[i], cmul(alpha, x[i]));
+}
+
+// ---- adjoint split-K + coil combine -------------------------------------
+// img[t,x,y] = sum_c conj(s_c[x,y]) * sum_s ws[s][t][c][x][y]
+// (kernels.py:158-172: out += conj(sens[c]) * part, coil order).
+__device__ __forceinline__ float2 coil_combine(const float2 *__restrict__ ws,
+                                               const float2 *__restrict__ sens,
+                                               int S, int T, int C, int64_t nxy,
+                                               int t, int64_t pix) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) {
+        float2 part = make_float2(0.f, 0.f);
+        for (int s = 0; s < S; ++s)
+            part = cadd(part, ws[(((int64_t)s * T + t) * C + c) * nxy + pix]);
+        acc = cadd(acc, cmulc(sens[(int64_t)c * nxy + pix], part));
+    }
+    return acc;
+}
+
+__global__ void k_adj_reduce(Geom g, int S, int C, const float2 *__restrict__ ws,
+                             const float2 *__restrict__ sens,
+                             float2 *__restrict__ out, const int *gate) {
+    if (gate && !*gate) return;
+    int64_t nxy = (int64_t)g.nx * g.ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t = (int)(i / nxy);
+        out[i] = coil_combine(ws, sens, S, g.T, C, nxy, t, i - t * nxy);
+    }
+}
+
+// out = fhf + (beta/2) Theta^H Theta x
+__global__ void k_normal_finish(Geom g, const float2 *__restrict__ fhf,
+                                const float2 *__restrict__ x, float hb,
+                                float2 *__restrict__ out) {
+    ThetaOf th{x, g};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t, xx, y;
+        unflat(g, i, t, xx, y);
+        float2 l = theta_adj_at(th, g, t, xx, y);
+        float2 f = fhf[i];
+        out[i] = make_float2(f.x + hb * l.x, f.y + hb * l.y);
+    }
+}
+
+// ---- native ADMM / CG loop ----------------------------------------------
+// Device-resident scalars; every kernel of an ADMM iteration is gated on
+// admm_active (and CG kernels on cg_active), which makes the iteration a
+// branch-free kernel sequence that is captured once as a CUDA graph.
+struct DevScalars {
+    double tau;                 // ||r||^2 (solver.py:106,117)
+    double alpha_re, alpha_im;  // CG step tau/<d,Ad> (solver.py:114)
+    double beta_cg;             // tau_next/tau (solver.py:121)
+    double admm_alpha;          // relative_change_sq (solver.py:149-155)
+    double atol2, rtol2;
+    int32_t cg_active, cg_iter, cg_max;
+    int32_t admm_active, admm_iter, admm_max;
+    int32_t cur;                // which rho buffer holds the current image
+    int32_t error;              // 1 = non-finite CG residual
+    float2 *snap;               // optional per-iteration image snapshots
+};
+
+struct IterLog {
+    int32_t iteration, cg_iterations;
+    double alpha, cg_final_residual_sq;
+};
+
+struct AdmmBufs {
+    float2 *rho[2];   // current image / CG solution (ping-pong)
+    float2 *mu, *eta; // (D, T, nx, ny)
+    float2 *fhd;      // F^H d
+    float2 *r, *d, *ad, *fhf;
+    double *partials;
+    unsigned *tickets;  // 4 tickets
+    DevScalars *s;
+    IterLog *log;
+    float t_s, t_t, hb;  // lam/beta, lam_t/beta, beta/2
+};
+
+// mu+ = S(theta(rho) + eta)  (solver.py:178)
+__global__ void k_admm_mu(Geom g, AdmmBufs b) {
+    if (!b.s->admm_active) return;
+    const float2 *rho = b.rho[b.s->cur];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int comp = (int)(i / g.n);
+        int t, x, y;
+        unflat(g, i - comp * g.n, t, x, y);
+        float2 v = cadd(theta_at(rho, g, comp, t, x, y), b.eta[i]);
+        b.mu[i] = soft1(v, comp == 2 ? b.t_t : b.t_s);
+    }
+}
+
+struct MuMinusEta {
+    const float2 *mu, *eta;
+    Geom g;
+    __device__ float2 operator()(int comp, int t, int x, int y) const {
+        int64_t i = comp * g.n + ((int64_t)t * g.nx + x) * g.ny + y;
+        return csub(mu[i], eta[i]);
+    }
+};
+
+// rhs = fhd + (beta/2) Theta^H (mu - eta) (solver.py:142-146); zero-start
+// CG init x = 0, r = d = rhs, tau = ||r||^2 (solver.py:99-108)
+__global__ void k_admm_rhs(Geom g, AdmmBufs b) {
+    if (!b.s->admm_active) return;
+    float2 *x = b.rho[b.s->cur ^ 1];
+    MuMinusEta u{b.mu, b.eta, g};
+    double v[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t, xx, y;
+        unflat(g, i, t, xx, y);
+        float2 l = theta_adj_at(u, g, t, xx, y);
+        float2 f = b.fhd[i];
+        float2 rhs = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+        x[i] = make_float2(0.f, 0.f);
+        b.r[i] = rhs;
+        b.d[i] = rhs;
+        v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
+    }
+    double tot[1];
+    if (grid_reduce<1>(v, b.partials, b.tickets + 0, tot) && threadIdx.x == 0) {
+        DevScalars *s = b.s;
+        double tau = tot[0];
+        s->tau = tau;
+        s->cg_iter = 0;
+        if (!isfinite(tau)) {
+            s->error = 1;
+            s->cg_active = 0;
+            s->admm_active = 0;
+        } else {
+            s->cg_active = (s->cg_max > 0 && tau > s->atol2) ? 1 : 0;
+        }
+    }
+}
+
+// ad = F^H F d (+ coil combine of split-K partials when ws != nullptr)
+//      + (beta/2) Theta^H Theta d ; <d, ad> -> alpha = tau / <d, ad>
+__global__ void k_cg_ad(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
+                        const float2 *__restrict__ sens, int S, int C) {
+    if (!b.s->cg_active) return;
+    ThetaOf th{b.d, g};
+    int64_t nxy = (int64_t)g.nx * g.ny;
+    double v[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t, xx, y;
+        unflat(g, i, t, xx, y);
+        float2 f = ws ? coil_combine(ws, sens, S, g.T, C, nxy, t, i - t * nxy)
+                      : b.fhf[i];
+        float2 l = theta_adj_at(th, g, t, xx, y);
+        float2 a = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+        b.ad[i] = a;
+        float2 d = b.d[i];
+        v[0] += (double)d.x * a.x + (double)d.y * a.y;
+        v[1] += (double)d.x * a.y - (double)d.y * a.x;
+    }
+    double tot[2];
+    if (grid_reduce<2>(v, b.partials, b.tickets + 1, tot) && threadIdx.x == 0) {
+        DevScalars *s = b.s;
+        double den = tot[0] * tot[0] + tot[1] * tot[1];
+        s->alpha_re = s->tau * tot[0] / den;
+        s->alpha_im = -s->tau * tot[1] / den;
+    }
+}
+
+// multi-GPU variant, first half: fhf = coil-combined partials (then the
+// allreduce runs on b.fhf, then k_cg_ad with ws == nullptr)
+__global__ void k_cg_fhf(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
+                         const float2 *__restrict__ sens, int S, int C) {
+    if (!b.s->cg_active) return;
+    int64_t nxy = (int64_t)g.nx * g.ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t = (int)(i / nxy);
+        b.fhf[i] = coil_combine(ws, sens, S, g.T, C, nxy, t, i - t * nxy);
+    }
+}
+
+// x += alpha d ; r -= alpha ad ; tau' = ||r||^2 (solver.py:115-122)
+__global__ void k_cg_xr(Geom g, AdmmBufs b) {
+    DevScalars *s = b.s;
+    if (!s->cg_active) return;
+    float2 *x = b.rho[s->cur ^ 1];
+    float2 al = make_float2((float)s->alpha_re, (float)s->alpha_im);
+    float2 nal = make_float2(-al.x, -al.y);
+    double v[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = cadd(x[i], cmul(al, b.d[i]));
+        float2 r = cadd(b.r[i], cmul(nal, b.ad[i]));
+        b.r[i] = r;
+        v[0] += (double)r.x * r.x + (double)r.y * r.y;
+    }
+    double tot[1];
+    if (grid_reduce<1>(v, b.partials, b.tickets + 2, tot) && threadIdx.x == 0) {
+        double tn = tot[0];
+        if (!isfinite(tn)) {
+            s->error = 1;
+            s->cg_active = 0;
+            s->admm_active = 0;
+            s->cg_iter += 1;
+            s->tau = tn;
+            return;
+        }
+        s->beta_cg = tn / s->tau;
+        s->tau = tn;
+        s->cg_iter += 1;
+        s->cg_active = (s->cg_iter < s->cg_max && tn > s->atol2) ? 1 : 0;
+    }
+}
+
+// d = r + (tau'/tau) d
+__global__ void k_cg_d(Geom g, AdmmBufs b) {
+    DevScalars *s = b.s;
+    if (!s->cg_active) return;
+    float be = (float)s->beta_cg;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 d = b.d[i], r = b.r[i];
+        b.d[i] = make_float2(r.x + be * d.x, r.y + be * d.y);
+    }
+}
+
+// eta+ = eta + (theta(rho+) - mu+) (solver.py:186); alpha = ||rho+ -
+// rho||^2 / ||rho||^2 (solver.py:149-155,192); loop guard
+// should_continue (solver.py:158-160); iteration record (solver.py:318-323)
+__global__ void k_admm_post(Geom g, AdmmBufs b) {
+    DevScalars *s = b.s;
+    if (!s->admm_active) return;
+    const float2 *rho = b.rho[s->cur];
+    const float2 *xn = b.rho[s->cur ^ 1];
+    double v[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int comp = (int)(i / g.n);
+        int64_t p = i - comp * g.n;
+        int t, x, y;
+        unflat(g, p, t, x, y);
+        float2 th = theta_at(xn, g, comp, t, x, y);
+        b.eta[i] = cadd(b.eta[i], csub(th, b.mu[i]));
+        if (comp == 0) {
+            float2 a = xn[p], o = rho[p];
+            float2 df = csub(a, o);
+            v[0] += (double)df.x * df.x + (double)df.y * df.y;
+            v[1] += (double)o.x * o.x + (double)o.y * o.y;
+        }
+    }
+    double tot[2];
+    if (grid_reduce<2>(v, b.partials, b.tickets + 3, tot) && threadIdx.x == 0) {
+        double num = tot[0], den = tot[1], alpha;
+        if (den > 0) alpha = num / den;
+        else alpha = num == 0 ? 0.0 : INFINITY;
+        s->admm_alpha = alpha;
+        IterLog &L = b.log[s->admm_iter];
+        L.iteration = s->admm_iter + 1;
+        L.cg_iterations = s->cg_iter;
+        L.alpha = alpha;
+        L.cg_final_residual_sq = s->tau;
+        s->admm_iter += 1;
+        s->cur ^= 1;
+        s->admm_active = (s->admm_iter < s->admm_max && alpha > s->rtol2 && !s->error) ? 1 : 0;
+    }
+}
+
+// snapshots[admm_iter] = rho[cur]; idempotent, so it needs no gate
+__global__ void k_snapshot(int64_t n, const DevScalars *s, const float2 *r0,
+                           const float2 *r1) {
+    float2 *dst = s->snap;
+    if (!dst) return;
+    dst += (int64_t)s->admm_iter * n;
+    const float2 *src = s->cur ? r1 : r0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+}  // namespace csr
