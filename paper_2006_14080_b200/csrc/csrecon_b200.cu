@@ -137,41 +137,49 @@ int check_device(int dev) {
     return CSR_OK;
 }
 
-// F x on the plan (x: (T,nx,ny) -> out (T*M, C))
+// F x on the plan: x (T,nx,ny) -> k-space.  out == nullptr keeps the result
+// in the plan's internal k-space buffer (what run_adjoint_partials(nullptr)
+// consumes); otherwise it is written as (T*M, C).
 int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
                 const int *gate) {
     if (p->tc.enabled) {
-        TRY(tc_forward(p->tc, x, p->sens, out, st, gate));
+        if (tc_forward(p->tc, x, out, st, gate)) return fail(CSR_ERR_CUDA, "tc forward launch");
         g_launches.fetch_add(p->tc.fwd_launches, std::memory_order_relaxed);
         return CSR_OK;
     }
     dim3 grid((unsigned)((p->M + ST - 1) / ST), (unsigned)p->C, (unsigned)p->T);
-    k_forward_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, p->sens, x, out, (int)p->M,
-                                         p->nx, p->ny, p->C, gate);
+    k_forward_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, p->sens, x, out ? out : p->kd,
+                                         (int)p->M, p->nx, p->ny, p->C, gate);
     LAUNCHED();
     return CSR_OK;
 }
 
-// split-K adjoint partials into p->ws (then coil-combined by a reduce kernel)
+// split-K adjoint partials into p->ws; kd == nullptr reads the internal
+// buffer written by run_forward(..., nullptr)
 int run_adjoint_partials(csr_plan *p, const float2 *kd, cudaStream_t st,
                          const int *gate) {
     if (p->tc.enabled) {
-        TRY(tc_adjoint(p->tc, kd, p->ws, st, gate));
-        g_launches.fetch_add(p->tc.adj_launches, std::memory_order_relaxed);
+        if (tc_adjoint(p->tc, kd, p->ws, st, gate)) return fail(CSR_ERR_CUDA, "tc adjoint launch");
+        g_launches.fetch_add(p->tc.adj_launches + (kd ? 1 : 0), std::memory_order_relaxed);
         return CSR_OK;
     }
     int tiles = ((p->nx + ST - 1) / ST) * ((p->ny + ST - 1) / ST);
     dim3 grid((unsigned)tiles, (unsigned)p->C, (unsigned)(p->T * p->S));
-    k_adjoint_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, kd, p->ws, (int)p->M, p->nx,
-                                         p->ny, p->C, p->T, p->kchunk, gate);
+    k_adjoint_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, kd ? kd : p->kd, p->ws, (int)p->M,
+                                         p->nx, p->ny, p->C, p->T, p->kchunk, gate);
     LAUNCHED();
     return CSR_OK;
 }
 
+// sens pointer for the coil combine of the split-K partials (nullptr when
+// the tensor-core epilogue already combined the coils)
+inline const float2 *combine_sens(const csr_plan *p) { return p->tc.enabled ? nullptr : p->sens; }
+inline int combine_coils(const csr_plan *p) { return p->tc.enabled ? 1 : p->C; }
+
 int run_adjoint(csr_plan *p, const float2 *kd, float2 *img, cudaStream_t st) {
     TRY(run_adjoint_partials(p, kd, st, nullptr));
-    k_adj_reduce<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->S, p->C, p->ws, p->sens,
-                                                    img, nullptr);
+    k_adj_reduce<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->S, combine_coils(p), p->ws,
+                                                    combine_sens(p), img, nullptr);
     LAUNCHED();
     return CSR_OK;
 }
@@ -218,16 +226,16 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     const int *gate = &p->sc->cg_active;
     const bool multi = p->comm && p->comm->nranks > 1;
     for (int it = 0; it < cg_max; ++it) {
-        TRY(run_forward(p, p->d, p->kd, st, gate));
+        TRY(run_forward(p, p->d, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.fwd_launches : 1;
-        TRY(run_adjoint_partials(p, p->kd, st, gate));
+        TRY(run_adjoint_partials(p, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.adj_launches : 1;
         if (multi) {
-            k_cg_fhf<<<eb, TPB, 0, st>>>(g, b, p->ws, p->sens, p->S, p->C); LAUNCHED(); ++k;
+            k_cg_fhf<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
             TRY(allreduce(p, p->fhf, g.n, st));
             k_cg_ad<<<eb, TPB, 0, st>>>(g, b, nullptr, p->sens, p->S, p->C); LAUNCHED(); ++k;
         } else {
-            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, p->ws, p->sens, p->S, p->C); LAUNCHED(); ++k;
+            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
         }
         k_cg_xr<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
         k_cg_d<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
@@ -312,7 +320,7 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     }
     // tensor-core operand build (returns tc.enabled=false for shapes it
     // does not tile; the SIMT kernels then handle the plan)
-    if ((rc = tc_plan_build(p->tc, p->T, p->nx, p->ny, p->C, p->M, p->P0, p->P1, st,
+    if ((rc = tc_plan_build(p->tc, p->T, p->nx, p->ny, p->C, p->M, p->P0, p->P1, p->sens, st,
                             &p->factor_bytes, &p->ws_bytes, p->allocs)))
         return cleanup(fail(rc, "tensor-core plan: " + g_err));
     // workspace
@@ -409,8 +417,8 @@ int csr_normal(csr_plan *p, const void *x, void *out, double beta, void *stream)
     if (!p || !x || !out) return fail(CSR_ERR_ARG, "null argument");
     CU(cudaSetDevice(p->dev));
     cudaStream_t st = (cudaStream_t)stream;
-    TRY(run_forward(p, (const float2 *)x, p->kd, st, nullptr));
-    TRY(run_adjoint(p, p->kd, p->fhf, st));
+    TRY(run_forward(p, (const float2 *)x, nullptr, st, nullptr));
+    TRY(run_adjoint(p, nullptr, p->fhf, st));
     k_normal_finish<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->fhf, (const float2 *)x,
                                                        (float)(beta / 2), (float2 *)out);
     LAUNCHED();

@@ -192,6 +192,10 @@ __device__ __forceinline__ float2 coil_combine(const float2 *__restrict__ ws,
                                                int S, int T, int C, int64_t nxy,
                                                int t, int64_t pix) {
     float2 acc = make_float2(0.f, 0.f);
+    if (!sens) {  // tensor-core partials: coils already combined
+        for (int s = 0; s < S; ++s) acc = cadd(acc, ws[((int64_t)s * T + t) * nxy + pix]);
+        return acc;
+    }
     for (int c = 0; c < C; ++c) {
         float2 part = make_float2(0.f, 0.f);
         for (int s = 0; s < S; ++s)

@@ -1,31 +1,880 @@
-// tcgen05 tensor-core NUDFT (placeholder until the tensor-core GEMMs land).
+// tcgen05 tensor-core separable NUDFT (K3 forward / K4 adjoint).
+//
+// Complex products are real GEMMs over an interleaved K axis: an operand
+// row holding complex values (re, im) along K multiplies a "doubled" row
+// pair [re, -im] / [im, re] of the other operand, giving Re and Im output
+// columns with no wasted MACs.  fp32 precision comes from a 3-term fp16
+// split (a = hi + lo, a*b ~ hi*hi + hi*lo + lo*hi, fp32 accumulation in
+// TMEM): 3 kind::f16 MMAs per K step.  Operands that are not unit-modulus
+// are scaled by an exact power of two so they sit well inside fp16 range.
+//
+// Layouts (all fp16, K-major, rows of 128 bytes per K block, TMA SWIZZLE_128B):
+//   forward A  fa[t*Mk + k][2y+{0,1}]          = P1[t][k][y]           (static)
+//   forward B  xb[t*Nf + 2(x*Cp+c)+part][2y+.] = [Xr,-Xi] / [Xi,Xr],   X = s_c*img_t
+//   adjoint A  ga[t*nyA + y][2k+{0,1}]         = conj(P1[t][k][y])     (static)
+//   adjoint B  generated in shared memory from P0 and d:
+//              row 2(x*Cp+c)+part, K (k, re/im):  W = sigma_d conj(P0[k,x]) d[k,c]
+// Forward epilogue (per sample k = TMEM lane): kd[k,c] = sum_x P0[k,x] G[k,(x,c)]
+// Adjoint epilogue (per pixel row y = TMEM lane): sum_c conj(s_c[x,y]) D[y,(x,c)],
+// written as split-K partial images ws[s][t][x][y].
 #pragma once
 
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace csr {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BN = 256;
+constexpr int TC_A_TILE = TC_BM * 128;   // 16 KiB
+constexpr int TC_B_TILE = TC_BN * 128;   // 32 KiB
+constexpr int TC_STAGES = 2;
+constexpr int TC_FWD_OPS = 2 * TC_A_TILE + 2 * TC_B_TILE;  // 96 KiB / stage
+constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
+constexpr int TC_ADJ_THREADS = 320;   // TMA, MMA, 4 epilogue, 4 generator warps
 
 struct TcPlan {
     bool enabled = false;
     int split = 1;
     float2 *ws = nullptr;
-    int fwd_launches = 0, adj_launches = 0;
+    int fwd_launches = 4, adj_launches = 1;
+    // geometry
+    int T = 1, nx = 0, ny = 0, C = 0;
+    int64_t M = 0, Mk = 0;
+    int Cp = 4, xs = 32, nxp = 0, nyp = 0, nyA = 0, Kf = 0, Nf = 0;
+    int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
+    int raw_bytes = 0, adj_stage = 0, fwd_smem = 0, adj_smem = 0;
+    // operands
+    __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
+    __half *xb_hi = nullptr, *xb_lo = nullptr;
+    float2 *p0p = nullptr, *kdp = nullptr, *kdi = nullptr;
+    const float2 *sens = nullptr;
+    float *scales = nullptr;  // [0]=sig_x [1]=1/sig_x [2]=sig_d [3]=1/sig_d [4]=max|s|
+    double *red = nullptr;
+    unsigned *tick = nullptr;
+    CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
 };
 
-inline int tc_plan_build(TcPlan &tc, int, int, int, int, int64_t, const float2 *,
-                         const float2 *, cudaStream_t, int64_t *, int64_t *,
-                         std::vector<void *> &) {
-    tc.enabled = false;
+// ---------------------------------------------------------------------------
+// small helpers
+__device__ __forceinline__ void split16(float v, __half &hi, __half &lo) {
+    hi = __float2half_rn(v);
+    lo = __float2half_rn(v - __half2float(hi));
+}
+__device__ __forceinline__ uint32_t pack2(__half a, __half b) {
+    return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
+__device__ __forceinline__ __half hneg(__half a) {
+    return __ushort_as_half(__half_as_ushort(a) ^ 0x8000u);
+}
+// exact power of two s with s * bound <= 2^14 (1 for bound == 0)
+__device__ __forceinline__ float pow2_scale(float bound) {
+    if (!(bound > 0.f) || !isfinite(bound)) return 1.f;
+    int e;
+    frexpf(bound, &e);  // bound = m * 2^e, m in [0.5, 1)
+    int s = 14 - e;
+    s = max(-120, min(120, s));
+    return ldexpf(1.f, s);
+}
+
+// deterministic grid max of non-negative values: true in thread 0 of the
+// last block to finish, with the maximum in `out`
+__device__ bool grid_max(float v, double *partials, unsigned *ticket, float &out) {
+    __shared__ float sh[32];
+    __shared__ int last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        float w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+        if (lane == 0) partials[blockIdx.x] = w;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (warp != 0) return false;
+    float w = 0.f;
+    for (unsigned b = lane; b < gridDim.x; b += 32) w = fmaxf(w, (float)__ldcg(partials + b));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+    if (lane != 0) return false;
+    *ticket = 0u;
+    out = w;
+    return true;
+}
+
+// scale pair (s, 1/s) for the operand bound factor * max
+__device__ void grid_max_scale(float v, double *partials, unsigned *ticket, float factor,
+                               float *out_scale) {
+    float m;
+    if (grid_max(v, partials, ticket, m)) {
+        const float s = pow2_scale(factor * m);
+        out_scale[0] = s;
+        out_scale[1] = 1.f / s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// setup kernels (plan build)
+__global__ void k_tc_build_fa(const float2 *__restrict__ P1, int T, int64_t M, int64_t Mk,
+                              int ny, int Kf, __half *hi, __half *lo) {
+    int64_t total = (int64_t)T * Mk * (Kf / 2);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int y = (int)(i % (Kf / 2));
+        int64_t r = i / (Kf / 2);
+        int64_t k = r % Mk;
+        int t = (int)(r / Mk);
+        float2 v = (k < M && y < ny) ? P1[((int64_t)t * M + k) * ny + y] : make_float2(0.f, 0.f);
+        __half h0, l0, h1, l1;
+        split16(v.x, h0, l0);
+        split16(v.y, h1, l1);
+        reinterpret_cast<uint32_t *>(hi)[i] = pack2(h0, h1);
+        reinterpret_cast<uint32_t *>(lo)[i] = pack2(l0, l1);
+    }
+}
+
+__global__ void k_tc_build_ga(const float2 *__restrict__ P1, int T, int64_t M, int64_t Mk,
+                              int ny, int nyA, __half *hi, __half *lo) {
+    int64_t total = (int64_t)T * nyA * Mk;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = i % Mk;
+        int64_t r = i / Mk;
+        int y = (int)(r % nyA);
+        int t = (int)(r / nyA);
+        float2 v = (k < M && y < ny) ? P1[((int64_t)t * M + k) * ny + y] : make_float2(0.f, 0.f);
+        __half h0, l0, h1, l1;
+        split16(v.x, h0, l0);
+        split16(-v.y, h1, l1);  // conj
+        reinterpret_cast<uint32_t *>(hi)[i] = pack2(h0, h1);
+        reinterpret_cast<uint32_t *>(lo)[i] = pack2(l0, l1);
+    }
+}
+
+__global__ void k_tc_build_p0(const float2 *__restrict__ P0, int T, int64_t M, int64_t Mk,
+                              int nx, int nxp, float2 *out) {
+    int64_t total = (int64_t)T * Mk * nxp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int x = (int)(i % nxp);
+        int64_t r = i / nxp;
+        int64_t k = r % Mk;
+        int t = (int)(r / Mk);
+        out[i] = (k < M && x < nx) ? P0[((int64_t)t * M + k) * nx + x] : make_float2(0.f, 0.f);
+    }
+}
+
+// scales[4] = max component magnitude of the coil maps
+__global__ void k_tc_sens_absmax(const float2 *__restrict__ s, int64_t n, double *partials,
+                                 unsigned *ticket, float *scales) {
+    float v = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v = fmaxf(v, fmaxf(fabsf(s[i].x), fabsf(s[i].y)));
+    float m;
+    if (grid_max(v, partials, ticket, m)) scales[4] = m;
+}
+
+// ---------------------------------------------------------------------------
+// per-application kernels
+struct TcArgs {
+    int T, nx, ny, C, Cp, xs, nxp, nyA, Kf, Nf;
+    int64_t M, Mk;
+};
+
+// sigma_x for the image operand X = s_c * img: bound = 2 max|s| max|img|
+__global__ void k_tc_absmax_img(const float2 *__restrict__ img, int64_t n, double *partials,
+                                unsigned *ticket, float *scales, const int *gate) {
+    if (gate && !*gate) return;
+    float v = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v = fmaxf(v, fmaxf(fabsf(img[i].x), fabsf(img[i].y)));
+    grid_max_scale(v, partials, ticket, 2.f * scales[4], scales + 0);
+}
+
+// X' = split(sigma_x * s_c * img_t) laid out as doubled rows (x, c, part)
+__global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
+                            const float2 *__restrict__ sens, const float *__restrict__ scales,
+                            __half *hi, __half *lo, const int *gate) {
+    if (gate && !*gate) return;
+    const float sg = scales[0];
+    const int hy = a.Kf / 2;  // complex y per row (nyp)
+    int64_t total = (int64_t)a.T * a.nxp * a.Cp * hy;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int y = (int)(i % hy);
+        int64_t r = i / hy;
+        int c = (int)(r % a.Cp);
+        r /= a.Cp;
+        int x = (int)(r % a.nxp);
+        int t = (int)(r / a.nxp);
+        float2 v = make_float2(0.f, 0.f);
+        if (x < a.nx && c < a.C && y < a.ny) {
+            int64_t p = (int64_t)x * a.ny + y;
+            v = cmul(sens[(int64_t)c * a.nx * a.ny + p], img[(int64_t)t * a.nx * a.ny + p]);
+            v.x *= sg;
+            v.y *= sg;
+        }
+        __half rh, rl, ih, il;
+        split16(v.x, rh, rl);
+        split16(v.y, ih, il);
+        int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)x * a.Cp + c);
+        int64_t e = row * (a.Kf / 2) + y;               // uint32 (half2) index
+        int64_t e1 = e + a.Kf / 2;                      // next row (Im part)
+        uint32_t *H = reinterpret_cast<uint32_t *>(hi), *L = reinterpret_cast<uint32_t *>(lo);
+        H[e] = pack2(rh, hneg(ih));
+        L[e] = pack2(rl, hneg(il));
+        H[e1] = pack2(ih, rh);
+        L[e1] = pack2(il, rl);
+    }
+}
+
+struct FwdParams {
+    TcArgs a;
+    int mt_per_frame, nt_per_group;
+    const float2 *p0p;
+    float2 *kdp;  // [G][T][Mk][Cp]
+    const float *scales;
+    const int *gate;
+};
+
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+    return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+template <int CP>
+__global__ void __launch_bounds__(TC_FWD_THREADS, 1)
+    k_tc_forward(const __grid_constant__ CUtensorMap tmA_hi,
+                 const __grid_constant__ CUtensorMap tmA_lo,
+                 const __grid_constant__ CUtensorMap tmB_hi,
+                 const __grid_constant__ CUtensorMap tmB_lo, FwdParams P) {
+    using namespace sm100;
+    if (P.gate && !*P.gate) return;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * TC_FWD_OPS);
+    uint64_t *empty = full + TC_STAGES;
+    uint64_t *tfull = empty + TC_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mtile = blockIdx.x;
+    const int t = mtile / P.mt_per_frame;
+    const int nt0 = blockIdx.y * P.nt_per_group, nt1 = nt0 + P.nt_per_group;
+    const int nkb = P.a.Kf / 64;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA_hi);
+        tma_prefetch(&tmA_lo);
+        tma_prefetch(&tmB_hi);
+        tma_prefetch(&tmB_lo);
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int nt = nt0; nt < nt1; ++nt) {
+                const int brow = t * P.a.Nf + nt * TC_BN;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % TC_STAGES;
+                    const uint32_t ph = (it / TC_STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *st = smem + s * TC_FWD_OPS;
+                    mbar_arrive_expect_tx(&full[s], TC_FWD_OPS);
+                    tma_load_2d(st, &tmA_hi, &full[s], kb * 64, mtile * TC_BM);
+                    tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, mtile * TC_BM);
+                    tma_load_2d(st + 2 * TC_A_TILE, &tmB_hi, &full[s], kb * 64, brow);
+                    tma_load_2d(st + 2 * TC_A_TILE + TC_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(TC_BM, TC_BN);
+            int it = 0, tc = 0;
+            for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+                const int ab = tc & 1;
+                const uint32_t aph = (tc >> 1) & 1;
+                mbar_wait(&tempty[ab], aph ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + ab * TC_BN;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % TC_STAGES;
+                    const uint32_t ph = (it / TC_STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * TC_FWD_OPS);
+                    const uint32_t a_hi = st, a_lo = st + TC_A_TILE;
+                    const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + TC_B_TILE;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t o = kk * 32;
+                        const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
+                        const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
+                        mma_f16(dcol, dah, dbh, idesc, (kb | kk) != 0);
+                        mma_f16(dcol, dah, dbl, idesc, 1);
+                        mma_f16(dcol, dal, dbh, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[ab]);
+            }
+        }
+    } else {
+        // epilogue: warps 2..5, TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int64_t kloc = (int64_t)(mtile % P.mt_per_frame) * TC_BM + row;
+        const bool valid = kloc < P.a.M;
+        const float2 *p0row = P.p0p + ((int64_t)t * P.a.Mk + kloc) * P.a.nxp;
+        constexpr int U = CP > 16 ? CP / 16 : 1;
+        float2 acc[CP];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) acc[c] = make_float2(0.f, 0.f);
+        int tc = 0;
+        for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+            const int ab = tc & 1;
+            const uint32_t aph = (tc >> 1) & 1;
+            mbar_wait(&tfull[ab], aph);
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + ab * TC_BN;
+            const int xbase = nt * P.a.xs;
+            for (int chb = 0; chb < 8; chb += U) {
+                float2 p0v[16 * U / CP > 0 ? 16 * U / CP : 1];
+#pragma unroll
+                for (int i = 0; i < 16 * U / CP; ++i) {
+                    const int x = xbase + (chb * 16) / CP + i;
+                    p0v[i] = valid ? p0row[x] : make_float2(0.f, 0.f);
+                }
+#pragma unroll
+                for (int h = 0; h < U; ++h) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + (chb + h) * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int jl = h * 16 + jj;
+                        const float2 gv = make_float2(__uint_as_float(r[2 * jj]),
+                                                      __uint_as_float(r[2 * jj + 1]));
+                        cfma(acc[jl % CP], p0v[jl / CP], gv);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+        }
+        if (valid) {
+            const float inv = P.scales[1];
+            float2 *out = P.kdp + (((int64_t)blockIdx.y * P.a.T + t) * P.a.Mk + kloc) * CP;
+#pragma unroll
+            for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// kd = sum_g kdp[g]; writes the internal padded layout (and optionally a
+// user (T*M, C) layout); sigma_d from max|kd|
+__global__ void k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, float2 *kdi,
+                            float2 *user, double *partials, unsigned *ticket, float *scales,
+                            const int *gate) {
+    if (gate && !*gate) return;
+    int64_t total = (int64_t)a.T * a.Mk * a.Cp;
+    int64_t gstride = total;
+    float v = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c = (int)(i % a.Cp);
+        int64_t r = i / a.Cp;
+        int64_t k = r % a.Mk;
+        int t = (int)(r / a.Mk);
+        float2 s = make_float2(0.f, 0.f);
+        if (k < a.M && c < a.C) {
+            for (int g = 0; g < G; ++g) s = cadd(s, kdp[g * gstride + i]);
+            v = fmaxf(v, fmaxf(fabsf(s.x), fabsf(s.y)));
+            if (user) user[((int64_t)t * a.M + k) * a.C + c] = s;
+        }
+        if (kdi) kdi[i] = s;
+    }
+    grid_max_scale(v, partials, ticket, 1.f, scales + 2);
+}
+
+// user (T*M, C) k-space -> internal padded layout + sigma_d
+__global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *kdi,
+                             double *partials, unsigned *ticket, float *scales) {
+    int64_t total = (int64_t)a.T * a.Mk * a.Cp;
+    float v = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c = (int)(i % a.Cp);
+        int64_t r = i / a.Cp;
+        int64_t k = r % a.Mk;
+        int t = (int)(r / a.Mk);
+        float2 s = make_float2(0.f, 0.f);
+        if (k < a.M && c < a.C) {
+            s = user[((int64_t)t * a.M + k) * a.C + c];
+            v = fmaxf(v, fmaxf(fabsf(s.x), fabsf(s.y)));
+        }
+        kdi[i] = s;
+    }
+    grid_max_scale(v, partials, ticket, 1.f, scales + 2);
+}
+
+struct AdjParams {
+    TcArgs a;
+    int S, kb_per_split, kb_total, raw_bytes, stage_bytes;
+    const float2 *sens;
+    float2 *ws;  // [S][T][nx][ny]
+    const float *scales;
+    const int *gate;
+};
+
+template <int CP>
+__global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
+    k_tc_adjoint(const __grid_constant__ CUtensorMap tmA_hi,
+                 const __grid_constant__ CUtensorMap tmA_lo,
+                 const __grid_constant__ CUtensorMap tmP0,
+                 const __grid_constant__ CUtensorMap tmKd, AdjParams P) {
+    using namespace sm100;
+    if (P.gate && !*P.gate) return;
+    constexpr int XS = 128 / CP;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * P.stage_bytes);
+    uint64_t *gen = full + TC_STAGES;
+    uint64_t *empty = gen + TC_STAGES;
+    uint64_t *tfull = empty + TC_STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = blockIdx.x, mt = blockIdx.y;
+    const int t = blockIdx.z % P.a.T, s_id = blockIdx.z / P.a.T;
+    const int kb0 = s_id * P.kb_per_split;
+    const int kb1 = min(P.kb_total, kb0 + P.kb_per_split);
+    const int nkb = kb1 - kb0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA_hi);
+        tma_prefetch(&tmA_lo);
+        tma_prefetch(&tmP0);
+        tma_prefetch(&tmKd);
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&gen[s], 4);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t raw_tx = 2 * TC_A_TILE + P.raw_bytes;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < nkb; ++i) {
+                const int kb = kb0 + i;
+                const int s = i % TC_STAGES;
+                const uint32_t ph = (i / TC_STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t *st = smem + s * P.stage_bytes;
+                uint8_t *raw = st + 2 * TC_A_TILE + 2 * TC_B_TILE;
+                mbar_arrive_expect_tx(&full[s], raw_tx);
+                const int arow = t * P.a.nyA + mt * TC_BM;
+                tma_load_2d(st, &tmA_hi, &full[s], kb * 64, arow);
+                tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, arow);
+                tma_load_3d(raw, &tmP0, &full[s], nt * XS, kb * 32, t);
+                tma_load_3d(raw + 32 * XS * 8, &tmKd, &full[s], 0, kb * 32, t);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(TC_BM, TC_BN);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % TC_STAGES;
+                const uint32_t ph = (i / TC_STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                mbar_wait(&gen[s], ph);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + s * P.stage_bytes);
+                const uint32_t a_hi = st, a_lo = st + TC_A_TILE;
+                const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + TC_B_TILE;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t o = kk * 32;
+                    const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
+                    const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
+                    mma_f16(tmem, dah, dbh, idesc, (i | kk) != 0);
+                    mma_f16(tmem, dah, dbl, idesc, 1);
+                    mma_f16(tmem, dal, dbh, idesc, 1);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(&tfull[0]);
+        }
+    } else if (warp >= 6) {
+        // generator: column j = (xl, c) of the B' tile, 32 samples per k block
+        const int j = threadIdx.x - 192;
+        const int xl = j / CP, c = j % CP;
+        const float sg = P.scales[2];
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % TC_STAGES;
+            const uint32_t ph = (i / TC_STAGES) & 1;
+            mbar_wait(&full[s], ph);
+            uint8_t *st = smem + s * P.stage_bytes;
+            const float2 *p0s = reinterpret_cast<const float2 *>(st + 2 * TC_A_TILE + 2 * TC_B_TILE);
+            const float2 *ds = p0s + 32 * XS;
+            uint8_t *bh = st + 2 * TC_A_TILE, *bl = bh + TC_B_TILE;
+            const uint32_t r_re = 2 * j, r_im = 2 * j + 1;
+#pragma unroll 2
+            for (int qq = 0; qq < 8; ++qq) {
+                const int q = (qq + j) & 7;  // rotate chunks to spread banks
+                __half wh[8], wl[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = 4 * q + u;
+                    const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
+                    const float wr = sg * (p.x * d.x + p.y * d.y);
+                    const float wi = sg * (p.x * d.y - p.y * d.x);
+                    split16(wr, wh[2 * u], wl[2 * u]);
+                    split16(wi, wh[2 * u + 1], wl[2 * u + 1]);
+                }
+                uint4 re_h, re_l, im_h, im_l;
+                re_h.x = pack2(wh[0], hneg(wh[1])); re_h.y = pack2(wh[2], hneg(wh[3]));
+                re_h.z = pack2(wh[4], hneg(wh[5])); re_h.w = pack2(wh[6], hneg(wh[7]));
+                re_l.x = pack2(wl[0], hneg(wl[1])); re_l.y = pack2(wl[2], hneg(wl[3]));
+                re_l.z = pack2(wl[4], hneg(wl[5])); re_l.w = pack2(wl[6], hneg(wl[7]));
+                im_h.x = pack2(wh[1], wh[0]); im_h.y = pack2(wh[3], wh[2]);
+                im_h.z = pack2(wh[5], wh[4]); im_h.w = pack2(wh[7], wh[6]);
+                im_l.x = pack2(wl[1], wl[0]); im_l.y = pack2(wl[3], wl[2]);
+                im_l.z = pack2(wl[5], wl[4]); im_l.w = pack2(wl[7], wl[6]);
+                *reinterpret_cast<uint4 *>(bh + sm100::sw128_off(r_re, q)) = re_h;
+                *reinterpret_cast<uint4 *>(bl + sm100::sw128_off(r_re, q)) = re_l;
+                *reinterpret_cast<uint4 *>(bh + sm100::sw128_off(r_im, q)) = im_h;
+                *reinterpret_cast<uint4 *>(bl + sm100::sw128_off(r_im, q)) = im_l;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gen[s]);
+        }
+    } else {
+        // epilogue: warps 2..5; TMEM lane = pixel row y
+        const int q = warp & 3;
+        const int yl = q * 32 + lane;
+        const int y = mt * TC_BM + yl;
+        const bool valid = y < P.a.ny;
+        constexpr int U = CP > 16 ? CP / 16 : 1;
+        mbar_wait(&tfull[0], 0);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+        const float inv = P.scales[3];
+        const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
+        float2 *wsp = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
+        for (int chb = 0; chb < 8; chb += U) {
+            float2 acc[16 * U / CP > 0 ? 16 * U / CP : 1];
+#pragma unroll
+            for (int i = 0; i < 16 * U / CP; ++i) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < U; ++h) {
+                uint32_t r[32];
+                tmem_ld32(taddr + (chb + h) * 32, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    const int jl = h * 16 + jj;
+                    const int c = jl % CP;
+                    const int x = nt * XS + (chb * 16 + jl) / CP;
+                    if (valid && c < P.a.C && x < P.a.nx) {
+                        const float2 dv = make_float2(__uint_as_float(r[2 * jj]),
+                                                      __uint_as_float(r[2 * jj + 1]));
+                        const float2 sv = P.sens[(int64_t)c * nxy + (int64_t)x * P.a.ny + y];
+                        acc[jl / CP] = cadd(acc[jl / CP], cmulc(sv, dv));
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 16 * U / CP; ++i) {
+                const int x = nt * XS + (chb * 16) / CP + i;
+                if (valid && x < P.a.nx)
+                    wsp[(int64_t)x * P.a.ny + y] = make_float2(acc[i].x * inv, acc[i].y * inv);
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+// 2-D fp16 K-major operand: inner dim K (elements), outer rows; box 64 x box_rows
+inline bool tmap_f16_2d(CUtensorMap *m, const void *base, uint64_t K, uint64_t rows,
+                        uint32_t box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {K, rows};
+    cuuint64_t strides[1] = {K * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D complex64 array viewed as 8-byte elements {d0, d1, d2}, no swizzle
+inline bool tmap_c64_3d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1,
+                        uint64_t d2, uint32_t b0, uint32_t b1) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+    cuuint32_t box[3] = {b0, b1, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void *>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline TcArgs tc_args(const TcPlan &tc) {
+    TcArgs a;
+    a.T = tc.T; a.nx = tc.nx; a.ny = tc.ny; a.C = tc.C; a.Cp = tc.Cp; a.xs = tc.xs;
+    a.nxp = tc.nxp; a.nyA = tc.nyA; a.Kf = tc.Kf; a.Nf = tc.Nf; a.M = tc.M; a.Mk = tc.Mk;
+    return a;
+}
+
+inline int tc_alloc(std::vector<void *> &allocs, void **p, size_t bytes, int64_t *acct) {
+    if (cudaMalloc(p, bytes ? bytes : 16) != cudaSuccess) return 2;
+    allocs.push_back(*p);
+    if (acct) *acct += (int64_t)bytes;
     return 0;
 }
-inline int tc_forward(TcPlan &, const float2 *, const float2 *, float2 *, cudaStream_t,
-                      const int *) {
-    return 3;
+
+template <class F>
+inline void set_smem(F kernel, int bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
-inline int tc_adjoint(TcPlan &, const float2 *, float2 *, cudaStream_t, const int *) {
-    return 3;
+
+inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
+                         const float2 *P0, const float2 *P1, const float2 *sens,
+                         cudaStream_t st, int64_t *factor_bytes, int64_t *ws_bytes,
+                         std::vector<void *> &allocs) {
+    tc.enabled = false;
+    if (C > 32 || getenv("CSR_DISABLE_TC")) return 0;
+    if (!get_encode()) return 0;
+    tc.T = T; tc.nx = nx; tc.ny = ny; tc.C = C; tc.M = M;
+    int Cp = 4;
+    while (Cp < C) Cp *= 2;
+    tc.Cp = Cp;
+    tc.xs = 128 / Cp;
+    tc.nxp = (nx + tc.xs - 1) / tc.xs * tc.xs;
+    tc.nyp = (ny + 31) / 32 * 32;
+    tc.nyA = (ny + 127) / 128 * 128;
+    tc.Kf = 2 * tc.nyp;
+    tc.Nf = 2 * tc.nxp * Cp;
+    tc.Mk = (M + 127) / 128 * 128;
+    tc.nt = tc.Nf / TC_BN;
+    tc.mt_f = (int)(tc.Mk / TC_BM);
+    // forward groups: split the n-tiles so the grid covers the machine
+    const int64_t mtiles = (int64_t)T * tc.mt_f;
+    int G = 1;
+    while (G < tc.nt && mtiles * G < 2 * 148 && tc.nt % (2 * G) == 0) G *= 2;
+    tc.G = G;
+    tc.nt_per_group = tc.nt / G;
+    // adjoint split-K
+    tc.mt_a = tc.nyA / TC_BM;
+    tc.kb_total = (int)(tc.Mk / 32);
+    const int64_t tiles = (int64_t)T * tc.mt_a * tc.nt;
+    int S = (int)std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+    S = std::min(S, std::max(1, tc.kb_total / 4));
+    tc.kb_per_split = (tc.kb_total + S - 1) / S;
+    S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
+    tc.split = S;
+    tc.raw_bytes = (32 * tc.xs * 8 + 32 * Cp * 8 + 1023) / 1024 * 1024;
+    tc.adj_stage = 2 * TC_A_TILE + 2 * TC_B_TILE + tc.raw_bytes;
+    tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
+    tc.adj_smem = TC_STAGES * tc.adj_stage + 1024 + 256;
+    if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
+
+    const size_t fa = (size_t)T * tc.Mk * tc.Kf, ga = (size_t)T * tc.nyA * 2 * tc.Mk;
+    const size_t xb = (size_t)T * tc.Nf * tc.Kf;
+    void *p;
+#define TCA(ptr, bytes, acct)                                 \
+    do {                                                      \
+        if (tc_alloc(allocs, &p, (bytes), (acct))) return 2;  \
+        ptr = decltype(ptr)(p);                               \
+    } while (0)
+    TCA(tc.fa_hi, fa * 2, factor_bytes);
+    TCA(tc.fa_lo, fa * 2, factor_bytes);
+    TCA(tc.ga_hi, ga * 2, factor_bytes);
+    TCA(tc.ga_lo, ga * 2, factor_bytes);
+    TCA(tc.p0p, (size_t)T * tc.Mk * tc.nxp * 8, factor_bytes);
+    TCA(tc.xb_hi, xb * 2, ws_bytes);
+    TCA(tc.xb_lo, xb * 2, ws_bytes);
+    TCA(tc.kdp, (size_t)G * T * tc.Mk * Cp * 8, ws_bytes);
+    TCA(tc.kdi, (size_t)T * tc.Mk * Cp * 8, ws_bytes);
+    TCA(tc.ws, (size_t)S * T * nx * ny * 8, ws_bytes);
+    TCA(tc.scales, 64, ws_bytes);
+    TCA(tc.red, 4 * 148 * 8, ws_bytes);
+    TCA(tc.tick, 64, ws_bytes);
+#undef TCA
+    tc.sens = sens;
+    cudaMemsetAsync(tc.tick, 0, 64, st);
+    const int blocks = 148 * 8;
+    k_tc_build_fa<<<blocks, 256, 0, st>>>(P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo);
+    k_tc_build_ga<<<blocks, 256, 0, st>>>(P1, T, M, tc.Mk, ny, tc.nyA, tc.ga_hi, tc.ga_lo);
+    k_tc_build_p0<<<blocks, 256, 0, st>>>(P0, T, M, tc.Mk, nx, tc.nxp, tc.p0p);
+    // max|s| (component-wise) for the image-operand scale bound
+    {
+        int64_t n = (int64_t)C * nx * ny;
+        int nb = reduce_blocks(n, 256);
+        k_tc_sens_absmax<<<nb, 256, 0, st>>>(sens, n, tc.red, tc.tick, tc.scales);
+    }
+    if (cudaGetLastError() != cudaSuccess) return 3;
+    bool ok = tmap_f16_2d(&tc.tm_fa_hi, tc.fa_hi, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
+              tmap_f16_2d(&tc.tm_fa_lo, tc.fa_lo, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
+              tmap_f16_2d(&tc.tm_xb_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
+              tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
+              tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
+              tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
+              tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, tc.xs, 32) &&
+              tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
+    if (!ok) return 0;  // descriptor encode unavailable: SIMT path
+    switch (Cp) {
+        case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem); break;
+        case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem); break;
+        case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
+        default: set_smem(k_tc_forward<32>, tc.fwd_smem); set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
+    }
+    tc.enabled = true;
+    return 0;
+}
+
+// image (T,nx,ny) -> kd.  user != nullptr: also write the (T*M, C) layout
+inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user,
+                      cudaStream_t st, const int *gate) {
+    TcArgs a = tc_args(tc);
+    const int64_t n = (int64_t)tc.T * tc.nx * tc.ny;
+    k_tc_absmax_img<<<reduce_blocks(n, 256), 256, 0, st>>>(img, n, tc.red, tc.tick, tc.scales,
+                                                           gate);
+    {
+        int64_t total = (int64_t)tc.T * tc.nxp * tc.Cp * tc.nyp;
+        int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+        k_tc_prep_x<<<nb, 256, 0, st>>>(a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate);
+    }
+    FwdParams P;
+    P.a = a;
+    P.mt_per_frame = tc.mt_f;
+    P.nt_per_group = tc.nt_per_group;
+    P.p0p = tc.p0p;
+    P.kdp = tc.kdp;
+    P.scales = tc.scales;
+    P.gate = gate;
+    dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)tc.G);
+    switch (tc.Cp) {
+        case 4: k_tc_forward<4><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+        case 8: k_tc_forward<8><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+        case 16: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+        default: k_tc_forward<32><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+    }
+    {
+        int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
+        k_tc_sum_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, tc.G, tc.kdp, tc.kdi, user,
+                                                               tc.red, tc.tick, tc.scales, gate);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// kd already in tc.kdi (with sigma_d) when user == nullptr; else load it
+inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t st,
+                      const int *gate) {
+    TcArgs a = tc_args(tc);
+    if (user) {
+        int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
+        k_tc_load_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, user, tc.kdi, tc.red, tc.tick,
+                                                                tc.scales);
+    }
+    AdjParams P;
+    P.a = a;
+    P.S = tc.split;
+    P.kb_per_split = tc.kb_per_split;
+    P.kb_total = tc.kb_total;
+    P.raw_bytes = tc.raw_bytes;
+    P.stage_bytes = tc.adj_stage;
+    P.sens = tc.sens;
+    P.ws = ws;
+    P.scales = tc.scales;
+    P.gate = gate;
+    dim3 grid((unsigned)tc.nt, (unsigned)tc.mt_a, (unsigned)(tc.T * tc.split));
+    switch (tc.Cp) {
+        case 4: k_tc_adjoint<4><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 8: k_tc_adjoint<8><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 16: k_tc_adjoint<16><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        default: k_tc_adjoint<32><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace csr
