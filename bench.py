@@ -312,7 +312,7 @@ def run_ours(args, cfg, world, rank, local):
     out = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * t_solve / args.steps, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "c64 (3xTF32 tensor GEMM, "
+           "scaling": "strong", "vs_baseline": None, "dtype": "c64 (tcgen05 fp16x3-split GEMM, "
            "fp32 accumulate)" if op.info()["gemm_path"] == "tcgen05" else "c64 (fp32 SIMT)",
            "data": "synthetic (seeded BASELINE generators; no public dataset)",
            "config": config_dict(cfg, world), "clocks": clk, "e2e": e2e,

@@ -39,6 +39,7 @@ constexpr int TC_STAGES = 2;
 constexpr int TC_FWD_OPS = 2 * TC_A_TILE + 2 * TC_B_TILE;  // 96 KiB / stage
 constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
 constexpr int TC_ADJ_THREADS = 320;   // TMA, MMA, 4 epilogue, 4 generator warps
+constexpr int TC_MAX_CHAIN = 24;      // max k blocks (32 samples) per adjoint CTA
 
 struct TcPlan {
     bool enabled = false;
@@ -503,7 +504,12 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
         mbar_init(&tfull[0], 1);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    // TMEM: [0,256) accumulates hi*hi, [256,512) the hi*lo + lo*hi
+    // corrections.  The tensor core's fp32 accumulation truncates on every
+    // MMA; keeping the small correction terms out of the main accumulator
+    // cuts the main chain's roundings 3x and makes the correction chain's
+    // truncation 2^-11 smaller ("accumulation precision").
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -545,8 +551,8 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
                     const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
                     const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
                     mma_f16(tmem, dah, dbh, idesc, (i | kk) != 0);
-                    mma_f16(tmem, dah, dbl, idesc, 1);
-                    mma_f16(tmem, dal, dbh, idesc, 1);
+                    mma_f16(tmem + TC_BN, dah, dbl, idesc, (i | kk) != 0);
+                    mma_f16(tmem + TC_BN, dal, dbh, idesc, 1);
                 }
                 mma_commit(&empty[s]);
             }
@@ -616,8 +622,9 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
             for (int i = 0; i < 16 * U / CP; ++i) acc[i] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int h = 0; h < U; ++h) {
-                uint32_t r[32];
+                uint32_t r[32], rc[32];
                 tmem_ld32(taddr + (chb + h) * 32, r);
+                tmem_ld32(taddr + TC_BN + (chb + h) * 32, rc);
                 tmem_ld_wait();
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
@@ -625,8 +632,9 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
                     const int c = jl % CP;
                     const int x = nt * XS + (chb * 16 + jl) / CP;
                     if (valid && c < P.a.C && x < P.a.nx) {
-                        const float2 dv = make_float2(__uint_as_float(r[2 * jj]),
-                                                      __uint_as_float(r[2 * jj + 1]));
+                        const float2 dv = make_float2(
+                            __uint_as_float(r[2 * jj]) + __uint_as_float(rc[2 * jj]),
+                            __uint_as_float(r[2 * jj + 1]) + __uint_as_float(rc[2 * jj + 1]));
                         const float2 sv = P.sens[(int64_t)c * nxy + (int64_t)x * P.a.ny + y];
                         acc[jl / CP] = cadd(acc[jl / CP], cmulc(sv, dv));
                     }
@@ -643,7 +651,7 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -749,6 +757,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     const int64_t tiles = (int64_t)T * tc.mt_a * tc.nt;
     int S = (int)std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
     S = std::min(S, std::max(1, tc.kb_total / 4));
+    // cap the per-CTA accumulation chain (truncating fp32 accumulate error
+    // grows linearly with the number of MMAs into one TMEM accumulator)
+    S = std::max(S, (tc.kb_total + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN);
+    if (const char *e = getenv("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
     tc.split = S;

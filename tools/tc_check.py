@@ -1,7 +1,7 @@
 """Quick tensor-core operator check vs the f64 oracle (dev tool)."""
 import sys, time
 import numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_2006_14080_b200 as P
 from oracle import csrecon_oracle as O
 
