@@ -23,6 +23,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -38,7 +40,6 @@ constexpr int TC_B_TILE = TC_BN * 128;   // 32 KiB
 constexpr int TC_STAGES = 2;
 constexpr int TC_FWD_OPS = 2 * TC_A_TILE + 2 * TC_B_TILE;  // 96 KiB / stage
 constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
-constexpr int TC_ADJ_THREADS = 320;   // TMA, MMA, 4 epilogue, 4 generator warps
 constexpr int TC_MAX_CHAIN = 24;      // max k blocks (32 samples) per adjoint CTA
 
 struct TcPlan {
@@ -344,8 +345,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                         const uint32_t o = kk * 32;
                         const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
                         const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
-                        mma_f16(dcol, dah, dbh, idesc, (kb | kk) != 0);
-                        mma_f16(dcol, dah, dbl, idesc, 1);
+                        mma_f16_fill(dcol, dah, dbh, idesc, (kb | kk) != 0);
+                        mma_f16_lastuse(dcol, dah, dbl, idesc, 1);
                         mma_f16(dcol, dal, dbh, idesc, 1);
                     }
                     mma_commit(&empty[s]);
@@ -460,43 +461,55 @@ __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *
 
 struct AdjParams {
     TcArgs a;
-    int S, kb_per_split, kb_total, raw_bytes, stage_bytes;
+    int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs;
     const float2 *sens;
     float2 *ws;  // [S][T][nx][ny]
     const float *scales;
     const int *gate;
 };
 
+// Adjoint, "A from TMEM" form.  Tile = 128 rows (x, c, part) of the generated
+// operand W' (64 complex (x, c) columns) x 128 pixel rows y, K = 32 samples
+// (64 fp16) per block.  The generator warps (which own TMEM lanes 0..127)
+// write W' straight into tensor memory with tcgen05.st, so shared memory only
+// carries the static factor conj(P1)^T (TMA, 128B swizzle) and the P0 / d
+// inputs of the generator: 4 stages deep.
+//   TMEM columns: [0,128) hi*hi accumulator, [128,256) hi*lo + lo*hi
+//   correction accumulator, [256,512) four A stages of (hi 32 | lo 32).
+constexpr int ADJ_STAGES = 4;
+constexpr int ADJ_B_TILE = 128 * 128;  // 16 KiB
+constexpr int ADJ_THREADS = 192;        // TMA, MMA, 4 generator/epilogue warps
+
 template <int CP>
-__global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
-    k_tc_adjoint(const __grid_constant__ CUtensorMap tmA_hi,
-                 const __grid_constant__ CUtensorMap tmA_lo,
+__global__ void __launch_bounds__(ADJ_THREADS, 1)
+    k_tc_adjoint(const __grid_constant__ CUtensorMap tmB_hi,
+                 const __grid_constant__ CUtensorMap tmB_lo,
                  const __grid_constant__ CUtensorMap tmP0,
                  const __grid_constant__ CUtensorMap tmKd, AdjParams P) {
     using namespace sm100;
     if (P.gate && !*P.gate) return;
-    constexpr int XS = 128 / CP;
+    constexpr int XS = 64 / CP;  // x values per tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * P.stage_bytes);
-    uint64_t *gen = full + TC_STAGES;
-    uint64_t *empty = gen + TC_STAGES;
-    uint64_t *tfull = empty + TC_STAGES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ADJ_STAGES * P.stage_bytes);
+    uint64_t *gen = full + ADJ_STAGES;
+    uint64_t *empty = gen + ADJ_STAGES;
+    uint64_t *tfull = empty + ADJ_STAGES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nt = blockIdx.x, mt = blockIdx.y;
+    const int mt = blockIdx.x, nt = blockIdx.y;
     const int t = blockIdx.z % P.a.T, s_id = blockIdx.z / P.a.T;
     const int kb0 = s_id * P.kb_per_split;
     const int kb1 = min(P.kb_total, kb0 + P.kb_per_split);
     const int nkb = kb1 - kb0;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&tmA_hi);
-        tma_prefetch(&tmA_lo);
+        tma_prefetch(&tmB_hi);
+        tma_prefetch(&tmB_lo);
         tma_prefetch(&tmP0);
         tma_prefetch(&tmKd);
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < ADJ_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&gen[s], 4);
             mbar_init(&empty[s], 1);
@@ -504,147 +517,137 @@ __global__ void __launch_bounds__(TC_ADJ_THREADS, 1)
         mbar_init(&tfull[0], 1);
         fence_barrier_init();
     }
-    // TMEM: [0,256) accumulates hi*hi, [256,512) the hi*lo + lo*hi
-    // corrections.  The tensor core's fp32 accumulation truncates on every
-    // MMA; keeping the small correction terms out of the main accumulator
-    // cuts the main chain's roundings 3x and makes the correction chain's
-    // truncation 2^-11 smaller ("accumulation precision").
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t raw_tx = 2 * TC_A_TILE + P.raw_bytes;
+    const uint32_t tx_bytes = 2 * ADJ_B_TILE + P.raw_bytes;
 
     if (warp == 0) {
         if (lane == 0) {
+            const int brow = t * P.a.nyA + nt * 128;
             for (int i = 0; i < nkb; ++i) {
                 const int kb = kb0 + i;
-                const int s = i % TC_STAGES;
-                const uint32_t ph = (i / TC_STAGES) & 1;
+                const int s = i % ADJ_STAGES;
+                const uint32_t ph = (i / ADJ_STAGES) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t *st = smem + s * P.stage_bytes;
-                uint8_t *raw = st + 2 * TC_A_TILE + 2 * TC_B_TILE;
-                mbar_arrive_expect_tx(&full[s], raw_tx);
-                const int arow = t * P.a.nyA + mt * TC_BM;
-                tma_load_2d(st, &tmA_hi, &full[s], kb * 64, arow);
-                tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, arow);
-                tma_load_3d(raw, &tmP0, &full[s], nt * XS, kb * 32, t);
+                uint8_t *raw = st + 2 * ADJ_B_TILE;
+                mbar_arrive_expect_tx(&full[s], tx_bytes);
+                tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
+                tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                tma_load_3d(raw, &tmP0, &full[s], mt * XS, kb * 32, t);
                 tma_load_3d(raw + 32 * XS * 8, &tmKd, &full[s], 0, kb * 32, t);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(TC_BM, TC_BN);
+            constexpr uint32_t idesc = idesc_f16(128, 128);
+            const uint32_t d_hi = tmem, d_lo = tmem + 128;
             for (int i = 0; i < nkb; ++i) {
-                const int s = i % TC_STAGES;
-                const uint32_t ph = (i / TC_STAGES) & 1;
+                const int s = i % ADJ_STAGES;
+                const uint32_t ph = (i / ADJ_STAGES) & 1;
                 mbar_wait(&full[s], ph);
                 mbar_wait(&gen[s], ph);
                 tc_fence_after();
                 const uint32_t st = smem_u32(smem + s * P.stage_bytes);
-                const uint32_t a_hi = st, a_lo = st + TC_A_TILE;
-                const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + TC_B_TILE;
+                const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t o = kk * 32;
-                    const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
-                    const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
-                    mma_f16(tmem, dah, dbh, idesc, (i | kk) != 0);
-                    mma_f16(tmem + TC_BN, dah, dbl, idesc, (i | kk) != 0);
-                    mma_f16(tmem + TC_BN, dal, dbh, idesc, 1);
+                    const uint64_t dbh = desc_sw128(st + kk * 32);
+                    const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
+                    mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, (i | kk) != 0);
+                    mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, (i | kk) != 0);
+                    mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
                 }
                 mma_commit(&empty[s]);
             }
             mma_commit(&tfull[0]);
         }
-    } else if (warp >= 6) {
-        // generator: column j = (xl, c) of the B' tile, 32 samples per k block
-        const int j = threadIdx.x - 192;
+    } else {
+        // warps 2..5 own TMEM lane quarter q = warp % 4: row m = (x, c, part)
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const float sg = P.scales[2];
+        // ---- generator: W' rows into the TMEM A stage
         for (int i = 0; i < nkb; ++i) {
-            const int s = i % TC_STAGES;
-            const uint32_t ph = (i / TC_STAGES) & 1;
+            const int s = i % ADJ_STAGES;
+            const uint32_t ph = (i / ADJ_STAGES) & 1;
             mbar_wait(&full[s], ph);
-            uint8_t *st = smem + s * P.stage_bytes;
-            const float2 *p0s = reinterpret_cast<const float2 *>(st + 2 * TC_A_TILE + 2 * TC_B_TILE);
+            const float2 *p0s = reinterpret_cast<const float2 *>(smem + s * P.stage_bytes +
+                                                                 2 * ADJ_B_TILE);
             const float2 *ds = p0s + 32 * XS;
-            uint8_t *bh = st + 2 * TC_A_TILE, *bl = bh + TC_B_TILE;
-            const uint32_t r_re = 2 * j, r_im = 2 * j + 1;
-#pragma unroll 2
-            for (int qq = 0; qq < 8; ++qq) {
-                const int q = (qq + j) & 7;  // rotate chunks to spread banks
-                __half wh[8], wl[8];
+            uint32_t hv[32], lv[32];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int k = 4 * q + u;
-                    const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
-                    const float wr = sg * (p.x * d.x + p.y * d.y);
-                    const float wi = sg * (p.x * d.y - p.y * d.x);
-                    split16(wr, wh[2 * u], wl[2 * u]);
-                    split16(wi, wh[2 * u + 1], wl[2 * u + 1]);
-                }
-                uint4 re_h, re_l, im_h, im_l;
-                re_h.x = pack2(wh[0], hneg(wh[1])); re_h.y = pack2(wh[2], hneg(wh[3]));
-                re_h.z = pack2(wh[4], hneg(wh[5])); re_h.w = pack2(wh[6], hneg(wh[7]));
-                re_l.x = pack2(wl[0], hneg(wl[1])); re_l.y = pack2(wl[2], hneg(wl[3]));
-                re_l.z = pack2(wl[4], hneg(wl[5])); re_l.w = pack2(wl[6], hneg(wl[7]));
-                im_h.x = pack2(wh[1], wh[0]); im_h.y = pack2(wh[3], wh[2]);
-                im_h.z = pack2(wh[5], wh[4]); im_h.w = pack2(wh[7], wh[6]);
-                im_l.x = pack2(wl[1], wl[0]); im_l.y = pack2(wl[3], wl[2]);
-                im_l.z = pack2(wl[5], wl[4]); im_l.w = pack2(wl[7], wl[6]);
-                *reinterpret_cast<uint4 *>(bh + sm100::sw128_off(r_re, q)) = re_h;
-                *reinterpret_cast<uint4 *>(bl + sm100::sw128_off(r_re, q)) = re_l;
-                *reinterpret_cast<uint4 *>(bh + sm100::sw128_off(r_im, q)) = im_h;
-                *reinterpret_cast<uint4 *>(bl + sm100::sw128_off(r_im, q)) = im_l;
+            for (int k = 0; k < 32; ++k) {
+                const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
+                const float wr = sg * (p.x * d.x + p.y * d.y);
+                const float wi = sg * (p.x * d.y - p.y * d.x);
+                // Re row (part 0): (wr, -wi); Im row (part 1): (wi, wr)
+                const float e0 = part ? wi : wr, e1 = part ? wr : -wi;
+                const __half2 hh = __floats2half2_rn(e0, e1);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(e0 - hf.x, e1 - hf.y);
+                hv[k] = *reinterpret_cast<const uint32_t *>(&hh);
+                lv[k] = *reinterpret_cast<const uint32_t *>(&ll);
             }
-            fence_proxy_async_smem();
+            tmem_st32(lane_base + 256 + 64 * s, hv);
+            tmem_st32(lane_base + 256 + 64 * s + 32, lv);
+            tmem_st_wait();
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[s]);
         }
-    } else {
-        // epilogue: warps 2..5; TMEM lane = pixel row y
-        const int q = warp & 3;
-        const int yl = q * 32 + lane;
-        const int y = mt * TC_BM + yl;
-        const bool valid = y < P.a.ny;
-        constexpr int U = CP > 16 ? CP / 16 : 1;
+        // ---- epilogue: D[(x,c,part), y] -> sum_c conj(s_c[x,y]) rho_c[x,y]
         mbar_wait(&tfull[0], 0);
         tc_fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
         const float inv = P.scales[3];
+        const int x = mt * XS + xl;
+        const bool ok = (x < P.a.nx) && (c < P.a.C);
         const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
-        float2 *wsp = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
-        for (int chb = 0; chb < 8; chb += U) {
-            float2 acc[16 * U / CP > 0 ? 16 * U / CP : 1];
+        const float2 *srow = P.sens + (int64_t)c * nxy + (int64_t)x * P.a.ny;
+        float2 *wrow = P.ws + ((int64_t)s_id * P.a.T + t) * nxy + (int64_t)x * P.a.ny;
+        const bool writer = ok && c == 0 && part == 0;
+        for (int cb = 0; cb < 4; ++cb) {
+            const int y0 = nt * 128 + cb * 32;
+            // coil-map segment for these 32 pixels, loaded up front so the
+            // global loads overlap (zero outside the image / padded coils)
+            float2 sv[32];
+            const float2 *sp = srow + y0;
+            if (ok && y0 + 32 <= P.a.ny && ((uintptr_t)sp & 15) == 0) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(sp);
 #pragma unroll
-            for (int i = 0; i < 16 * U / CP; ++i) acc[i] = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int h = 0; h < U; ++h) {
-                uint32_t r[32], rc[32];
-                tmem_ld32(taddr + (chb + h) * 32, r);
-                tmem_ld32(taddr + TC_BN + (chb + h) * 32, rc);
-                tmem_ld_wait();
-#pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                    const int jl = h * 16 + jj;
-                    const int c = jl % CP;
-                    const int x = nt * XS + (chb * 16 + jl) / CP;
-                    if (valid && c < P.a.C && x < P.a.nx) {
-                        const float2 dv = make_float2(
-                            __uint_as_float(r[2 * jj]) + __uint_as_float(rc[2 * jj]),
-                            __uint_as_float(r[2 * jj + 1]) + __uint_as_float(rc[2 * jj + 1]));
-                        const float2 sv = P.sens[(int64_t)c * nxy + (int64_t)x * P.a.ny + y];
-                        acc[jl / CP] = cadd(acc[jl / CP], cmulc(sv, dv));
-                    }
+                for (int u = 0; u < 16; ++u) {
+                    const float4 f = __ldg(s4 + u);
+                    sv[2 * u] = make_float2(f.x, f.y);
+                    sv[2 * u + 1] = make_float2(f.z, f.w);
                 }
-            }
+            } else {
 #pragma unroll
-            for (int i = 0; i < 16 * U / CP; ++i) {
-                const int x = nt * XS + (chb * 16) / CP + i;
-                if (valid && x < P.a.nx)
-                    wsp[(int64_t)x * P.a.ny + y] = make_float2(acc[i].x * inv, acc[i].y * inv);
+                for (int u = 0; u < 32; ++u)
+                    sv[u] = (ok && y0 + u < P.a.ny) ? sp[u] : make_float2(0.f, 0.f);
+            }
+            uint32_t rh[32], rl[32];
+            tmem_ld32(lane_base + cb * 32, rh);
+            tmem_ld32(lane_base + 128 + cb * 32, rl);
+            tmem_ld_wait();
+#pragma unroll
+            for (int yy = 0; yy < 32; ++yy) {
+                const float v = (__uint_as_float(rh[yy]) + __uint_as_float(rl[yy])) * inv;
+                const float o = __shfl_xor_sync(0xffffffffu, v, 1);
+                const float re = part ? o : v, im = part ? v : o;
+                float pr = sv[yy].x * re + sv[yy].y * im;  // conj(s) * rho
+                float pi = sv[yy].x * im - sv[yy].y * re;
+#pragma unroll
+                for (int off = 2; off < 2 * CP; off <<= 1) {
+                    pr += __shfl_xor_sync(0xffffffffu, pr, off);
+                    pi += __shfl_xor_sync(0xffffffffu, pi, off);
+                }
+                if (writer && y0 + yy < P.a.ny) wrow[y0 + yy] = make_float2(pr, pi);
             }
         }
     }
@@ -730,7 +733,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
                          cudaStream_t st, int64_t *factor_bytes, int64_t *ws_bytes,
                          std::vector<void *> &allocs) {
     tc.enabled = false;
-    if (C > 32 || getenv("CSR_DISABLE_TC")) return 0;
+    if (C > 16 || getenv("CSR_DISABLE_TC")) return 0;
     if (!get_encode()) return 0;
     tc.T = T; tc.nx = nx; tc.ny = ny; tc.C = C; tc.M = M;
     int Cp = 4;
@@ -752,22 +755,36 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.G = G;
     tc.nt_per_group = tc.nt / G;
     // adjoint split-K
-    tc.mt_a = tc.nyA / TC_BM;
+    tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
-    const int64_t tiles = (int64_t)T * tc.mt_a * tc.nt;
+    const int64_t tiles = (int64_t)T * tc.mt_a * (tc.nyA / 128);
     int S = (int)std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
     S = std::min(S, std::max(1, tc.kb_total / 4));
     // cap the per-CTA accumulation chain (truncating fp32 accumulate error
     // grows linearly with the number of MMAs into one TMEM accumulator)
     S = std::max(S, (tc.kb_total + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN);
+    {
+        // among S .. 2S pick the split minimising (waves of 148 CTAs) x chain
+        int best = S;
+        int64_t best_cost = INT64_MAX;
+        for (int c = S; c <= std::min(2 * S, tc.kb_total); ++c) {
+            const int64_t chain = (tc.kb_total + c - 1) / c;
+            const int64_t waves = (tiles * c + 147) / 148;
+            if (waves * chain < best_cost) {
+                best_cost = waves * chain;
+                best = c;
+            }
+        }
+        S = best;
+    }
     if (const char *e = getenv("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
     tc.split = S;
-    tc.raw_bytes = (32 * tc.xs * 8 + 32 * Cp * 8 + 1023) / 1024 * 1024;
-    tc.adj_stage = 2 * TC_A_TILE + 2 * TC_B_TILE + tc.raw_bytes;
+    tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
+    tc.adj_stage = (2 * ADJ_B_TILE + tc.raw_bytes + 1023) / 1024 * 1024;
     tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
-    tc.adj_smem = TC_STAGES * tc.adj_stage + 1024 + 256;
+    tc.adj_smem = ADJ_STAGES * tc.adj_stage + 1024 + 256;
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
     const size_t fa = (size_t)T * tc.Mk * tc.Kf, ga = (size_t)T * tc.nyA * 2 * tc.Mk;
@@ -811,14 +828,14 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
               tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
-              tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, tc.xs, 32) &&
+              tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
               tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
     if (!ok) return 0;  // descriptor encode unavailable: SIMT path
     switch (Cp) {
         case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem); break;
         case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem); break;
         case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
-        default: set_smem(k_tc_forward<32>, tc.fwd_smem); set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
+        default: break;
     }
     tc.enabled = true;
     return 0;
@@ -848,8 +865,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user,
     switch (tc.Cp) {
         case 4: k_tc_forward<4><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
         case 8: k_tc_forward<8><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-        case 16: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-        default: k_tc_forward<32><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+        default: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
     }
     {
         int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
@@ -875,16 +891,16 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
     P.stage_bytes = tc.adj_stage;
+    P.xs = 64 / tc.Cp;
     P.sens = tc.sens;
     P.ws = ws;
     P.scales = tc.scales;
     P.gate = gate;
-    dim3 grid((unsigned)tc.nt, (unsigned)tc.mt_a, (unsigned)(tc.T * tc.split));
+    dim3 grid((unsigned)tc.mt_a, (unsigned)(tc.nyA / 128), (unsigned)(tc.T * tc.split));
     switch (tc.Cp) {
-        case 4: k_tc_adjoint<4><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 8: k_tc_adjoint<8><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 16: k_tc_adjoint<16><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        default: k_tc_adjoint<32><<<grid, TC_ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 4: k_tc_adjoint<4><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 8: k_tc_adjoint<8><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        default: k_tc_adjoint<16><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
     }
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
