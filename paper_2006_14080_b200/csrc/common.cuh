@@ -84,6 +84,25 @@ __device__ bool grid_reduce(double (&v)[NV], double *partials,
     return true;
 }
 
+// Plan buffers come from the device's default stream-ordered pool with an
+// unbounded release threshold, so building and dropping plans (one per
+// reconstruction call) reuses memory instead of paying cudaMalloc/cudaFree
+// (and the device-wide sync of cudaFree) every time.
+inline cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !configured[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured[dev] = true;
+    }
+    return cudaMallocAsync(p, bytes ? bytes : 16, st);
+}
+
 // Grid size used by every reduction kernel over n elements: a function of n
 // only, so reductions are run-to-run deterministic.
 inline int reduce_blocks(int64_t n, int threads) {

@@ -107,7 +107,7 @@ int dalloc(csr_plan *p, T **ptr, size_t count, int64_t *acct) {
     size_t bytes = count * sizeof(T);
     if (bytes == 0) bytes = 16;
     void *v = nullptr;
-    cudaError_t e = cudaMalloc(&v, bytes);
+    cudaError_t e = pool_alloc(&v, bytes, p->stream);
     if (e != cudaSuccess)
         return fail(CSR_ERR_OOM, std::string("cudaMalloc(") + std::to_string(bytes) +
                                      "): " + cudaGetErrorString(e));
@@ -292,18 +292,18 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         return rc;
     };
     int rc;
-    if ((rc = dalloc(p, &p->P0, (size_t)(rows * p->nx), &p->factor_bytes))) return cleanup(rc);
-    if ((rc = dalloc(p, &p->P1, (size_t)(rows * p->ny), &p->factor_bytes))) return cleanup(rc);
-    if ((rc = dalloc(p, &p->sens, (size_t)(p->C * nxy), &p->factor_bytes))) return cleanup(rc);
     cudaStream_t st;
     if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, "stream create failed"));
     p->stream = st;
+    if ((rc = dalloc(p, &p->P0, (size_t)(rows * p->nx), &p->factor_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->P1, (size_t)(rows * p->ny), &p->factor_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->sens, (size_t)(p->C * nxy), &p->factor_bytes))) return cleanup(rc);
     for (auto &e : p->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "event create"));
     // coords -> device, factors in f64 -> complex64
     double *dcoords = nullptr;
-    if (cudaMalloc(&dcoords, rows * 2 * sizeof(double)) != cudaSuccess)
+    if (pool_alloc((void **)&dcoords, rows * 2 * sizeof(double), st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_OOM, "coords alloc"));
     p->allocs.push_back(dcoords);
     if (cudaMemcpyAsync(dcoords, desc->coords, rows * 2 * sizeof(double),
@@ -370,8 +370,9 @@ int csr_plan_destroy(csr_plan *p) {
     cudaSetDevice(p->dev);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
-    for (void *a : p->allocs) cudaFree(a);
-    if (p->log) cudaFree(p->log);
+    for (void *a : p->allocs) cudaFreeAsync(a, p->stream);
+    if (p->log) cudaFreeAsync(p->log, p->stream);
+    if (p->stream) cudaStreamSynchronize(p->stream);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : p->iter_ev) cudaEventDestroy(e);
@@ -526,9 +527,9 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     const Geom g = p->g;
     const int64_t n = g.n, nD = g.n * g.D;
     if (p->log_cap < prm->admm_max_iters) {
-        if (p->log) cudaFree(p->log);
+        if (p->log) cudaFreeAsync(p->log, st);
         p->log = nullptr;
-        CU(cudaMalloc(&p->log, sizeof(IterLog) * prm->admm_max_iters));
+        CU(pool_alloc((void **)&p->log, sizeof(IterLog) * prm->admm_max_iters, st));
         p->log_cap = prm->admm_max_iters;
         if (p->graph) {
             cudaGraphExecDestroy(p->graph);

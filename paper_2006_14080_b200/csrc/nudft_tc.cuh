@@ -40,7 +40,7 @@ constexpr int TC_B_TILE = TC_BN * 128;   // 32 KiB
 constexpr int TC_STAGES = 2;
 constexpr int TC_FWD_OPS = 2 * TC_A_TILE + 2 * TC_B_TILE;  // 96 KiB / stage
 constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
-constexpr int TC_MAX_CHAIN = 24;      // max k blocks (32 samples) per adjoint CTA
+constexpr int TC_MAX_CHAIN = 24;      // max k blocks (32 samples) per accumulation chain
 
 struct TcPlan {
     bool enabled = false;
@@ -461,25 +461,31 @@ __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *
 
 struct AdjParams {
     TcArgs a;
-    int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs;
+    int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs, chain;
     const float2 *sens;
     float2 *ws;  // [S][T][nx][ny]
     const float *scales;
     const int *gate;
 };
 
-// Adjoint, "A from TMEM" form.  Tile = 128 rows (x, c, part) of the generated
-// operand W' (64 complex (x, c) columns) x 128 pixel rows y, K = 32 samples
-// (64 fp16) per block.  The generator warps (which own TMEM lanes 0..127)
-// write W' straight into tensor memory with tcgen05.st, so shared memory only
-// carries the static factor conj(P1)^T (TMA, 128B swizzle) and the P0 / d
-// inputs of the generator: 4 stages deep.
-//   TMEM columns: [0,128) hi*hi accumulator, [128,256) hi*lo + lo*hi
-//   correction accumulator, [256,512) four A stages of (hi 32 | lo 32).
 constexpr int ADJ_STAGES = 4;
-constexpr int ADJ_B_TILE = 128 * 128;  // 16 KiB
-constexpr int ADJ_THREADS = 192;        // TMA, MMA, 4 generator/epilogue warps
+constexpr int ADJ_B_TILE = 128 * 128;   // 16 KiB
+constexpr int ADJ_THREADS = 384;        // WG0: TMA, MMA; WG1: generator; WG2: epilogue
+constexpr int ADJ_SUM_BYTES = 128 * 128 * 4;  // fp32 running sum [y][lane]
 
+// Adjoint, "A from TMEM" form, one tile x one contiguous k range per CTA.
+// Tile = 128 rows (x, c, part) of the generated operand W' (64 complex
+// (x, c) columns) x 128 pixel rows y; K = 32 samples (64 fp16) per block.
+// The generator warpgroup writes W' straight into tensor memory with
+// tcgen05.st, so shared memory only carries the static factor conj(P1)^T
+// (TMA, 128B swizzle) and the P0 / d inputs of the generator (4 stages).
+// The k range is cut into accumulation chains of <= chain blocks (the
+// tensor core truncates on every fp32 accumulate); the epilogue warpgroup
+// drains each chain into an fp32 running sum in shared memory and frees the
+// accumulator, and after the last chain combines coils and writes one
+// split-K partial image.
+//   TMEM columns: [0,128) hi*hi accumulator, [128,256) hi*lo + lo*hi
+//   corrections, [256,512) four A stages of (hi 32 | lo 32).
 template <int CP>
 __global__ void __launch_bounds__(ADJ_THREADS, 1)
     k_tc_adjoint(const __grid_constant__ CUtensorMap tmB_hi,
@@ -491,11 +497,14 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     constexpr int XS = 64 / CP;  // x values per tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ADJ_STAGES * P.stage_bytes);
+    float *sum_s = reinterpret_cast<float *>(smem + ADJ_STAGES * P.stage_bytes);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ADJ_STAGES * P.stage_bytes +
+                                                  ADJ_SUM_BYTES);
     uint64_t *gen = full + ADJ_STAGES;
     uint64_t *empty = gen + ADJ_STAGES;
-    uint64_t *tfull = empty + ADJ_STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+    uint64_t *acc_full = empty + ADJ_STAGES;
+    uint64_t *acc_empty = acc_full + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x, nt = blockIdx.y;
@@ -503,6 +512,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     const int kb0 = s_id * P.kb_per_split;
     const int kb1 = min(P.kb_total, kb0 + P.kb_per_split);
     const int nkb = kb1 - kb0;
+    const int chain = P.chain;
+    const int nchain = (nkb + chain - 1) / chain;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmB_hi);
@@ -514,7 +525,8 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             mbar_init(&gen[s], 4);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(&tfull[0], 1);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -545,35 +557,41 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, 128);
             const uint32_t d_hi = tmem, d_lo = tmem + 128;
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % ADJ_STAGES;
-                const uint32_t ph = (i / ADJ_STAGES) & 1;
-                mbar_wait(&full[s], ph);
-                mbar_wait(&gen[s], ph);
+            int i = 0;
+            for (int ch = 0; ch < nchain; ++ch) {
+                mbar_wait(acc_empty, (ch & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t st = smem_u32(smem + s * P.stage_bytes);
-                const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
+                const int iend = min(nkb, i + chain);
+                for (int i0 = i; i < iend; ++i) {
+                    const int s = i % ADJ_STAGES;
+                    const uint32_t ph = (i / ADJ_STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    mbar_wait(&gen[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * P.stage_bytes);
+                    const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t dbh = desc_sw128(st + kk * 32);
-                    const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
-                    mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, (i | kk) != 0);
-                    mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, (i | kk) != 0);
-                    mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t dbh = desc_sw128(st + kk * 32);
+                        const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
+                        const uint32_t acc = (i != i0) || (kk != 0);
+                        mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, acc);
+                        mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, acc);
+                        mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);
                 }
-                mma_commit(&empty[s]);
+                mma_commit(acc_full);
             }
-            mma_commit(&tfull[0]);
         }
-    } else {
-        // warps 2..5 own TMEM lane quarter q = warp % 4: row m = (x, c, part)
+    } else if (warp >= 4 && warp < 8) {
+        // ---- generator warpgroup: lane quarter q, row m = (x, c, part)
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const float sg = P.scales[2];
-        // ---- generator: W' rows into the TMEM A stage
         for (int i = 0; i < nkb; ++i) {
             const int s = i % ADJ_STAGES;
             const uint32_t ph = (i / ADJ_STAGES) & 1;
@@ -602,10 +620,37 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[s]);
         }
-        // ---- epilogue: D[(x,c,part), y] -> sum_c conj(s_c[x,y]) rho_c[x,y]
-        mbar_wait(&tfull[0], 0);
-        tc_fence_after();
+    } else if (warp >= 8) {
+        // ---- epilogue warpgroup
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int j = m >> 1, part = m & 1;
+        const int xl = j / CP, c = j % CP;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const float inv = P.scales[3];
+        for (int ch = 0; ch < nchain; ++ch) {
+            mbar_wait(acc_full, ch & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < 4; ++cb) {
+                uint32_t rh[32], rl[32];
+                tmem_ld32(lane_base + cb * 32, rh);
+                tmem_ld32(lane_base + 128 + cb * 32, rl);
+                tmem_ld_wait();
+                if (cb == 3) {  // accumulator fully read: let the MMA go on
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty);
+                }
+#pragma unroll
+                for (int yy = 0; yy < 32; ++yy) {
+                    const float v = __uint_as_float(rh[yy]) + __uint_as_float(rl[yy]);
+                    float *dst = sum_s + (cb * 32 + yy) * 128 + m;
+                    *dst = ch ? *dst + v : v;
+                }
+            }
+        }
+        // ---- D[(x,c,part), y] -> sum_c conj(s_c[x,y]) rho_c[x,y]
         const int x = mt * XS + xl;
         const bool ok = (x < P.a.nx) && (c < P.a.C);
         const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
@@ -614,8 +659,6 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         const bool writer = ok && c == 0 && part == 0;
         for (int cb = 0; cb < 4; ++cb) {
             const int y0 = nt * 128 + cb * 32;
-            // coil-map segment for these 32 pixels, loaded up front so the
-            // global loads overlap (zero outside the image / padded coils)
             float2 sv[32];
             const float2 *sp = srow + y0;
             if (ok && y0 + 32 <= P.a.ny && ((uintptr_t)sp & 15) == 0) {
@@ -631,13 +674,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 for (int u = 0; u < 32; ++u)
                     sv[u] = (ok && y0 + u < P.a.ny) ? sp[u] : make_float2(0.f, 0.f);
             }
-            uint32_t rh[32], rl[32];
-            tmem_ld32(lane_base + cb * 32, rh);
-            tmem_ld32(lane_base + 128 + cb * 32, rl);
-            tmem_ld_wait();
 #pragma unroll
             for (int yy = 0; yy < 32; ++yy) {
-                const float v = (__uint_as_float(rh[yy]) + __uint_as_float(rl[yy])) * inv;
+                const float v = sum_s[(cb * 32 + yy) * 128 + m] * inv;
                 const float o = __shfl_xor_sync(0xffffffffu, v, 1);
                 const float re = part ? o : v, im = part ? v : o;
                 float pr = sv[yy].x * re + sv[yy].y * im;  // conj(s) * rho
@@ -716,8 +755,9 @@ inline TcArgs tc_args(const TcPlan &tc) {
     return a;
 }
 
-inline int tc_alloc(std::vector<void *> &allocs, void **p, size_t bytes, int64_t *acct) {
-    if (cudaMalloc(p, bytes ? bytes : 16) != cudaSuccess) return 2;
+inline int tc_alloc(std::vector<void *> &allocs, void **p, size_t bytes, int64_t *acct,
+                    cudaStream_t st) {
+    if (pool_alloc(p, bytes, st) != cudaSuccess) return 2;
     allocs.push_back(*p);
     if (acct) *acct += (int64_t)bytes;
     return 0;
@@ -758,24 +798,25 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
     const int64_t tiles = (int64_t)T * tc.mt_a * (tc.nyA / 128);
-    int S = (int)std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
-    S = std::min(S, std::max(1, tc.kb_total / 4));
-    // cap the per-CTA accumulation chain (truncating fp32 accumulate error
-    // grows linearly with the number of MMAs into one TMEM accumulator)
-    S = std::max(S, (tc.kb_total + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN);
+    // split-K: each CTA takes one tile and a contiguous k range, cut into
+    // accumulation chains of <= TC_MAX_CHAIN blocks.  Pick S by a cost model
+    // (waves of 148 CTAs x per-CTA time: blocks x ~768 MMA cycles + chain
+    // drains + CTA setup/fill), bounded by the partial-image memory.
+    int S = 1;
     {
-        // among S .. 2S pick the split minimising (waves of 148 CTAs) x chain
-        int best = S;
+        const int64_t pix = (int64_t)T * nx * ny * 8;
         int64_t best_cost = INT64_MAX;
-        for (int c = S; c <= std::min(2 * S, tc.kb_total); ++c) {
-            const int64_t chain = (tc.kb_total + c - 1) / c;
+        for (int c = 1; c <= std::min(tc.kb_total, 1024); ++c) {
+            if (c > 1 && c * pix > ((int64_t)1 << 30)) break;
+            const int64_t kbps = (tc.kb_total + c - 1) / c;
+            const int64_t nch = (kbps + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN;
             const int64_t waves = (tiles * c + 147) / 148;
-            if (waves * chain < best_cost) {
-                best_cost = waves * chain;
-                best = c;
+            const int64_t cost = waves * (kbps * 768 + nch * 700 + 4000);
+            if (cost < best_cost) {
+                best_cost = cost;
+                S = c;
             }
         }
-        S = best;
     }
     if (const char *e = getenv("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
@@ -784,7 +825,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
     tc.adj_stage = (2 * ADJ_B_TILE + tc.raw_bytes + 1023) / 1024 * 1024;
     tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
-    tc.adj_smem = ADJ_STAGES * tc.adj_stage + 1024 + 256;
+    tc.adj_smem = ADJ_STAGES * tc.adj_stage + ADJ_SUM_BYTES + 1024 + 256;
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
     const size_t fa = (size_t)T * tc.Mk * tc.Kf, ga = (size_t)T * tc.nyA * 2 * tc.Mk;
@@ -792,7 +833,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     void *p;
 #define TCA(ptr, bytes, acct)                                 \
     do {                                                      \
-        if (tc_alloc(allocs, &p, (bytes), (acct))) return 2;  \
+        if (tc_alloc(allocs, &p, (bytes), (acct), st)) return 2;  \
         ptr = decltype(ptr)(p);                               \
     } while (0)
     TCA(tc.fa_hi, fa * 2, factor_bytes);
@@ -888,6 +929,7 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.a = a;
     P.S = tc.split;
     P.kb_per_split = tc.kb_per_split;
+    P.chain = TC_MAX_CHAIN;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
     P.stage_bytes = tc.adj_stage;
