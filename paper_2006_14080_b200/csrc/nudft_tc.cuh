@@ -52,7 +52,7 @@ struct TcPlan {
     int64_t M = 0, Mk = 0;
     int Cp = 4, xs = 32, nxp = 0, nyp = 0, nyA = 0, Kf = 0, Nf = 0;
     int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
-    int raw_bytes = 0, adj_stage = 0, fwd_smem = 0, adj_smem = 0;
+    int raw_bytes = 0, adj_stage = 0, fwd_smem = 0, adj_smem = 0, adj_cs = 1;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
@@ -256,6 +256,12 @@ struct FwdParams {
     const float *scales;
     const int *gate;
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
     return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
@@ -462,6 +468,8 @@ __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *
 struct AdjParams {
     TcArgs a;
     int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs, chain;
+    int exp_flags;  // profiling experiments: 1 = no generator math, 2 = no MMA
+    int cs;         // cluster size along the (x, c) tiles sharing one B tile
     const float2 *sens;
     float2 *ws;  // [S][T][nx][ny]
     const float *scales;
@@ -471,7 +479,8 @@ struct AdjParams {
 constexpr int ADJ_STAGES = 4;
 constexpr int ADJ_B_TILE = 128 * 128;   // 16 KiB
 constexpr int ADJ_THREADS = 384;        // WG0: TMA, MMA; WG1: generator; WG2: epilogue
-constexpr int ADJ_SUM_BYTES = 128 * 128 * 4;  // fp32 running sum [y][lane]
+constexpr int ADJ_SUM_LD = 129;                       // padded row (floats)
+constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 running sums [y][lane]
 
 // Adjoint, "A from TMEM" form, one tile x one contiguous k range per CTA.
 // Tile = 128 rows (x, c, part) of the generated operand W' (64 complex
@@ -523,7 +532,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         for (int s = 0; s < ADJ_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&gen[s], 4);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], P.cs);  // every cluster CTA's MMA frees stage s
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
@@ -532,9 +541,14 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
+    if (P.cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tx_bytes = 2 * ADJ_B_TILE + P.raw_bytes;
+    const uint32_t tx_bytes = ((P.exp_flags & 8) ? 0 : 2 * ADJ_B_TILE) +
+                              ((P.exp_flags & 16) ? 0 : P.raw_bytes);
+    const uint32_t crank = P.cs > 1 ? cluster_ctarank() : 0;
+
+    const uint16_t cmask = (uint16_t)((1u << P.cs) - 1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -547,10 +561,23 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 uint8_t *st = smem + s * P.stage_bytes;
                 uint8_t *raw = st + 2 * ADJ_B_TILE;
                 mbar_arrive_expect_tx(&full[s], tx_bytes);
-                tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
-                tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
-                tma_load_3d(raw, &tmP0, &full[s], mt * XS, kb * 32, t);
-                tma_load_3d(raw + 32 * XS * 8, &tmKd, &full[s], 0, kb * 32, t);
+                if (P.exp_flags & 8) {
+                } else if (P.cs > 1) {
+                    // this CTA fetches rows [crank*R, (crank+1)*R) of the shared
+                    // B tile and multicasts them to the whole cluster
+                    const int R = 128 / P.cs;
+                    tma_load_2d_mc(st + crank * R * 128, &tmB_hi, &full[s], kb * 64,
+                                   brow + crank * R, cmask);
+                    tma_load_2d_mc(st + ADJ_B_TILE + crank * R * 128, &tmB_lo, &full[s],
+                                   kb * 64, brow + crank * R, cmask);
+                } else {
+                    tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
+                    tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                }
+                if (!(P.exp_flags & 16)) {
+                    tma_load_3d(raw, &tmP0, &full[s], mt * XS, kb * 32, t);
+                    tma_load_3d(raw + 32 * XS * 8, &tmKd, &full[s], 0, kb * 32, t);
+                }
             }
         }
     } else if (warp == 1) {
@@ -575,11 +602,14 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                         const uint64_t dbh = desc_sw128(st + kk * 32);
                         const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
                         const uint32_t acc = (i != i0) || (kk != 0);
+                        if (P.exp_flags & 2) continue;
                         mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, acc);
                         mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, acc);
                         mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
                     }
-                    mma_commit(&empty[s]);
+                    if (P.exp_flags & 32) mbar_arrive(&empty[s]);
+                    else if (P.cs > 1) mma_commit_mc(&empty[s], cmask);
+                    else mma_commit(&empty[s]);
                 }
                 mma_commit(acc_full);
             }
@@ -600,6 +630,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                                                                  2 * ADJ_B_TILE);
             const float2 *ds = p0s + 32 * XS;
             uint32_t hv[32], lv[32];
+            if (P.exp_flags & 1) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) hv[k] = lv[k] = 0u;
+            } else
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
@@ -613,9 +647,11 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 hv[k] = *reinterpret_cast<const uint32_t *>(&hh);
                 lv[k] = *reinterpret_cast<const uint32_t *>(&ll);
             }
-            tmem_st32(lane_base + 256 + 64 * s, hv);
-            tmem_st32(lane_base + 256 + 64 * s + 32, lv);
-            tmem_st_wait();
+            if (!(P.exp_flags & 4)) {
+                tmem_st32(lane_base + 256 + 64 * s, hv);
+                tmem_st32(lane_base + 256 + 64 * s + 32, lv);
+                tmem_st_wait();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[s]);
@@ -645,52 +681,48 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
 #pragma unroll
                 for (int yy = 0; yy < 32; ++yy) {
                     const float v = __uint_as_float(rh[yy]) + __uint_as_float(rl[yy]);
-                    float *dst = sum_s + (cb * 32 + yy) * 128 + m;
+                    float *dst = sum_s + (cb * 32 + yy) * ADJ_SUM_LD + m;
                     *dst = ch ? *dst + v : v;
                 }
             }
         }
-        // ---- D[(x,c,part), y] -> sum_c conj(s_c[x,y]) rho_c[x,y]
-        const int x = mt * XS + xl;
-        const bool ok = (x < P.a.nx) && (c < P.a.C);
-        const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
-        const float2 *srow = P.sens + (int64_t)c * nxy + (int64_t)x * P.a.ny;
-        float2 *wrow = P.ws + ((int64_t)s_id * P.a.T + t) * nxy + (int64_t)x * P.a.ny;
-        const bool writer = ok && c == 0 && part == 0;
-        for (int cb = 0; cb < 4; ++cb) {
-            const int y0 = nt * 128 + cb * 32;
-            float2 sv[32];
-            const float2 *sp = srow + y0;
-            if (ok && y0 + 32 <= P.a.ny && ((uintptr_t)sp & 15) == 0) {
-                const float4 *s4 = reinterpret_cast<const float4 *>(sp);
+        // ---- combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y)
+        // thread e handles pixel row y = e for every x of the tile, reading the
+        // transposed sums (padded rows: conflict-free) and the coil maps with
+        // y-coalesced loads
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (P.exp_flags & 64) goto done;
+        {
+            const int e = threadIdx.x - 256;
+            const int y = nt * 128 + e;
+            const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
+            float2 *wbase = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
+            const float *row = sum_s + e * ADJ_SUM_LD;
+            if (y < P.a.ny) {
+#pragma unroll 2
+                for (int xq = 0; xq < XS; ++xq) {
+                    const int xg = mt * XS + xq;
+                    if (xg >= P.a.nx) break;
+                    float ar = 0.f, ai = 0.f;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const float4 f = __ldg(s4 + u);
-                    sv[2 * u] = make_float2(f.x, f.y);
-                    sv[2 * u + 1] = make_float2(f.z, f.w);
+                    for (int cc = 0; cc < CP; ++cc) {
+                        if (cc < P.a.C) {
+                            const float re = row[2 * (xq * CP + cc)];
+                            const float im = row[2 * (xq * CP + cc) + 1];
+                            const float2 sv = __ldg(P.sens + (int64_t)cc * nxy +
+                                                    (int64_t)xg * P.a.ny + y);
+                            ar += sv.x * re + sv.y * im;
+                            ai += sv.x * im - sv.y * re;
+                        }
+                    }
+                    wbase[(int64_t)xg * P.a.ny + y] = make_float2(ar * inv, ai * inv);
                 }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    sv[u] = (ok && y0 + u < P.a.ny) ? sp[u] : make_float2(0.f, 0.f);
-            }
-#pragma unroll
-            for (int yy = 0; yy < 32; ++yy) {
-                const float v = sum_s[(cb * 32 + yy) * 128 + m] * inv;
-                const float o = __shfl_xor_sync(0xffffffffu, v, 1);
-                const float re = part ? o : v, im = part ? v : o;
-                float pr = sv[yy].x * re + sv[yy].y * im;  // conj(s) * rho
-                float pi = sv[yy].x * im - sv[yy].y * re;
-#pragma unroll
-                for (int off = 2; off < 2 * CP; off <<= 1) {
-                    pr += __shfl_xor_sync(0xffffffffu, pr, off);
-                    pi += __shfl_xor_sync(0xffffffffu, pi, off);
-                }
-                if (writer && y0 + yy < P.a.ny) wrow[y0 + yy] = make_float2(pr, pi);
             }
         }
+    done:;
     }
     __syncthreads();
+    if (P.cs > 1) cluster_sync();  // no CTA leaves while peers may still signal it
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -823,6 +855,12 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
     tc.split = S;
     tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
+    // clusters of CTAs that share one B tile (same frame, split, y tile)
+    tc.adj_cs = tc.mt_a % 4 == 0 ? 4 : (tc.mt_a % 2 == 0 ? 2 : 1);
+    if (const char *e = getenv("CSR_ADJ_CLUSTER")) {
+        int v = atoi(e);
+        if ((v == 1 || v == 2 || v == 4) && tc.mt_a % v == 0) tc.adj_cs = v;
+    }
     tc.adj_stage = (2 * ADJ_B_TILE + tc.raw_bytes + 1023) / 1024 * 1024;
     tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
     tc.adj_smem = ADJ_STAGES * tc.adj_stage + ADJ_SUM_BYTES + 1024 + 256;
@@ -867,8 +905,8 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_fa_lo, tc.fa_lo, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
               tmap_f16_2d(&tc.tm_xb_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
-              tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
-              tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, TC_BM) &&
+              tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
+              tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
               tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
     if (!ok) return 0;  // descriptor encode unavailable: SIMT path
@@ -930,6 +968,8 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.S = tc.split;
     P.kb_per_split = tc.kb_per_split;
     P.chain = TC_MAX_CHAIN;
+    P.exp_flags = getenv("CSR_EXP") ? atoi(getenv("CSR_EXP")) : 0;
+    P.cs = tc.adj_cs;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
     P.stage_bytes = tc.adj_stage;
@@ -939,11 +979,25 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.scales = tc.scales;
     P.gate = gate;
     dim3 grid((unsigned)tc.mt_a, (unsigned)(tc.nyA / 128), (unsigned)(tc.T * tc.split));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(ADJ_THREADS);
+    cfg.dynamicSmemBytes = tc.adj_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = tc.adj_cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
     switch (tc.Cp) {
-        case 4: k_tc_adjoint<4><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 8: k_tc_adjoint<8><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        default: k_tc_adjoint<16><<<grid, ADJ_THREADS, tc.adj_smem, st>>>(tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<8>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
     }
+    if (e != cudaSuccess) return 3;
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
