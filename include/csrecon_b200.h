@@ -65,8 +65,13 @@ typedef struct csr_plan_desc {
     const double *coords; /* HOST, (T*M, 2) */
     const void *sens;     /* DEVICE complex64 (C, nx, ny); copied */
     int32_t device;       /* CUDA ordinal */
-    int32_t reserved;
+    int32_t flags;        /* CSR_PLAN_FRAME_SHARD: this plan holds a contiguous
+                             block of the frames of a 2-D+t problem split across
+                             ranks; temporal differences at the block edges use
+                             halo frames exchanged with the neighbour ranks */
 } csr_plan_desc;
+
+#define CSR_PLAN_FRAME_SHARD 1
 
 typedef struct csr_plan_info {
     int64_t factor_bytes;    /* resident encoding factors */

@@ -25,7 +25,9 @@ class PlanDesc(ctypes.Structure):
                 ("n_samples", ctypes.c_int64),
                 ("coords", ctypes.POINTER(ctypes.c_double)),
                 ("sens", ctypes.c_void_p), ("device", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("flags", ctypes.c_int32)]
+
+CSR_PLAN_FRAME_SHARD = 1
 
 
 class PlanInfo(ctypes.Structure):

@@ -92,6 +92,10 @@ struct csr_plan {
     int kernels_per_iter = 0;
     csr_comm *comm = nullptr;
     int64_t factor_bytes = 0, ws_bytes = 0;
+    // frame sharding (CSR_PLAN_FRAME_SHARD): halo frames and scalar slots
+    bool frame_mode = false;
+    float2 *hprev = nullptr, *hnext = nullptr, *sfirst = nullptr, *slast = nullptr;
+    double *loc = nullptr;
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
     int64_t flush_bytes = 0;
@@ -191,6 +195,49 @@ int allreduce(csr_plan *p, float2 *buf, int64_t n_complex, cudaStream_t st) {
     return CSR_OK;
 }
 
+int nranks(const csr_plan *p) { return p->comm ? p->comm->nranks : 1; }
+
+// frame-sharded plans finalise CG/ADMM scalars after an allreduce of the
+// per-rank sums (CSR_FORCE_MR exercises that path on one GPU)
+bool multi_rank_scalars(const csr_plan *p) {
+    return p->frame_mode && (nranks(p) > 1 || getenv("CSR_FORCE_MR"));
+}
+
+// Ring halo exchange of one frame each way: hprev <- previous rank's `last`,
+// hnext <- next rank's `first` (ranks in frame order, circular like the
+// temporal difference).  One rank: local copies.
+int halo_exchange(csr_plan *p, const float2 *first, const float2 *last, cudaStream_t st) {
+    const size_t nb = (size_t)p->nx * p->ny * sizeof(float2);
+    const int P = nranks(p);
+    if (P == 1) {
+        CU(cudaMemcpyAsync(p->hprev, last, nb, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(p->hnext, first, nb, cudaMemcpyDeviceToDevice, st));
+        return CSR_OK;
+    }
+    const int r = p->comm->rank, nxt = (r + 1) % P, prv = (r + P - 1) % P;
+    const size_t nf = 2 * (size_t)p->nx * p->ny;
+    NC(ncclGroupStart());
+    NC(ncclSend(last, nf, ncclFloat, nxt, p->comm->comm, st));
+    NC(ncclRecv(p->hprev, nf, ncclFloat, prv, p->comm->comm, st));
+    NC(ncclSend(first, nf, ncclFloat, prv, p->comm->comm, st));
+    NC(ncclRecv(p->hnext, nf, ncclFloat, nxt, p->comm->comm, st));
+    NC(ncclGroupEnd());
+    return CSR_OK;
+}
+
+// multi-rank scalars: allreduce the local sums, then the scalar update
+int scalar_sync(csr_plan *p, const AdmmBufs &b, int op, int off, int cnt, cudaStream_t st,
+                int *nk) {
+    if (!b.mr) return CSR_OK;
+    if (nranks(p) > 1)
+        NC(ncclAllReduce(p->loc + off, p->loc + off, (size_t)cnt, ncclDouble, ncclSum,
+                         p->comm->comm, st));
+    k_finalize<<<1, 1, 0, st>>>(b, op);
+    LAUNCHED();
+    ++*nk;
+    return CSR_OK;
+}
+
 AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
     AdmmBufs b;
     b.rho[0] = p->rho[0];
@@ -212,6 +259,11 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
     double lt = prm->lam_t > 0 ? prm->lam_t : prm->lam;
     b.t_t = (float)(lt / prm->beta);
     b.hb = (float)(prm->beta / 2);
+    b.mr = multi_rank_scalars(p) ? 1 : 0;
+    b.loc = p->loc;
+    b.hprev = p->hprev;
+    b.hnext = p->hnext;
+    b.sfirst = p->sfirst;
     return b;
 }
 
@@ -220,27 +272,44 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
                            cudaStream_t st, int *nk) {
     const Geom g = p->g;
     const int eb = ew_blocks(g.n), ebD = ew_blocks(g.n * g.D);
+    const int ebf = ew_blocks((int64_t)g.nx * g.ny);
+    const bool fm = p->frame_mode;
     int k = 0;
+    if (fm) {  // rho halos for theta(rho)
+        k_stage_frames<<<ebf, TPB, 0, st>>>(b, g, 0, p->sfirst, p->slast); LAUNCHED(); ++k;
+        TRY(halo_exchange(p, p->sfirst, p->slast, st));
+    }
     k_admm_mu<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    if (fm) TRY(halo_exchange(p, p->sfirst, p->sfirst, st));  // next rank's (mu-eta)_t[0]
     k_admm_rhs<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    TRY(scalar_sync(p, b, FIN_RHS, 0, 1, st, &k));
     const int *gate = &p->sc->cg_active;
-    const bool multi = p->comm && p->comm->nranks > 1;
+    const bool coil_multi = !fm && p->comm && p->comm->nranks > 1;
+    const int64_t nf = (int64_t)g.nx * g.ny;
     for (int it = 0; it < cg_max; ++it) {
+        if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
         TRY(run_forward(p, p->d, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.fwd_launches : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.adj_launches : 1;
-        if (multi) {
+        if (coil_multi) {
             k_cg_fhf<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
             TRY(allreduce(p, p->fhf, g.n, st));
             k_cg_ad<<<eb, TPB, 0, st>>>(g, b, nullptr, p->sens, p->S, p->C); LAUNCHED(); ++k;
         } else {
             k_cg_ad<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
         }
+        TRY(scalar_sync(p, b, FIN_AD, 1, 2, st, &k));
         k_cg_xr<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+        TRY(scalar_sync(p, b, FIN_XR, 3, 1, st, &k));
         k_cg_d<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
     }
+    if (fm) {  // halos of the new image for theta(rho+)
+        k_stage_frames<<<ebf, TPB, 0, st>>>(b, g, 1, p->sfirst, p->slast); LAUNCHED(); ++k;
+        TRY(halo_exchange(p, p->sfirst, p->slast, st));
+    }
     k_admm_post<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    TRY(scalar_sync(p, b, FIN_POST, 4, 2, st, &k));
     k_snapshot<<<eb, TPB, 0, st>>>(g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
     *nk = k;
     return CSR_OK;
@@ -285,6 +354,11 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     p->C = desc->n_coils;
     p->M = desc->n_samples;
     p->g = make_geom(p->T, p->nx, p->ny);
+    if (desc->flags & CSR_PLAN_FRAME_SHARD) {
+        p->frame_mode = true;
+        p->g.halo = 1;
+        p->g.D = 3;  // a frame block of a 2-D+t problem (even a single frame)
+    }
     const int64_t rows = (int64_t)p->T * p->M;
     const int64_t nxy = (int64_t)p->nx * p->ny;
     auto cleanup = [&](int rc) {
@@ -354,6 +428,13 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     if ((rc = dalloc(p, &p->d, (size_t)n, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->ad, (size_t)n, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->partials, (size_t)(4 * 148 * 4), &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->loc, 8, &p->ws_bytes))) return cleanup(rc);
+    if (p->frame_mode) {
+        if ((rc = dalloc(p, &p->hprev, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
+        if ((rc = dalloc(p, &p->hnext, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
+        if ((rc = dalloc(p, &p->sfirst, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
+        if ((rc = dalloc(p, &p->slast, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
+    }
     if ((rc = dalloc(p, &p->tickets, 8, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->sc, 1, &p->ws_bytes))) return cleanup(rc);
     if (cudaMemsetAsync(p->tickets, 0, 8 * sizeof(unsigned), st) != cudaSuccess)
@@ -543,7 +624,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     CU(cudaEventRecord(p->ev[0], st));
     TRY(run_adjoint(p, (const float2 *)kdata, p->fhd, st));
     CU(cudaMemcpyAsync(p->rho[0], p->fhd, n * sizeof(float2), cudaMemcpyDeviceToDevice, st));
-    if (p->comm && p->comm->nranks > 1) {
+    if (!p->frame_mode && p->comm && p->comm->nranks > 1) {
         TRY(allreduce(p, p->rho[0], n, st));
         TRY(allreduce(p, p->fhd, n, st));
         ar_calls += 2;
@@ -567,7 +648,8 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     AdmmBufs b = admm_bufs(p, prm);
     std::vector<double> key = {prm->lam, prm->lam_t, prm->beta,
                                (double)prm->cg_max_iters,
-                               (double)(p->comm ? p->comm->nranks : 1)};
+                               (double)(p->comm ? p->comm->nranks : 1),
+                               (double)(b.mr)};
     bool use_graph = true;
     if (!p->graph || p->graph_key != key) {
         if (p->graph) {
@@ -647,7 +729,8 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         int cg_total = 0;
         for (int i = 0; i < hs.admm_iter; ++i) cg_total += hl[i].cg_iterations;
         if (hs.error) cg_total += hs.cg_iter;
-        stats->allreduce_calls = ar_calls + ((p->comm && p->comm->nranks > 1) ? cg_total : 0);
+        stats->allreduce_calls =
+            ar_calls + ((!p->frame_mode && p->comm && p->comm->nranks > 1) ? cg_total : 0);
         stats->setup_ms = ms_setup;
         stats->solve_ms = ms_solve;
         if (timed) {

@@ -15,6 +15,8 @@ struct Geom {
     int T, nx, ny;
     int64_t n;   // T*nx*ny
     int D;       // theta components
+    int halo;    // 1: frame-sharded, temporal neighbours of frames 0 / T-1
+                 // come from halo buffers instead of wrapping locally
 };
 
 __host__ __device__ inline Geom make_geom(int T, int nx, int ny) {
@@ -22,6 +24,7 @@ __host__ __device__ inline Geom make_geom(int T, int nx, int ny) {
     g.T = T; g.nx = nx; g.ny = ny;
     g.n = (int64_t)T * nx * ny;
     g.D = T > 1 ? 3 : 2;
+    g.halo = 0;
     return g;
 }
 
@@ -56,14 +59,19 @@ __global__ void k_factors(const double *__restrict__ coords, int64_t rows,
 }
 
 // ---- circular finite differences ----------------------------------------
+// hprev (halo mode): the previous rank's last frame, used as frame -1
 __device__ __forceinline__ float2 theta_at(const float2 *__restrict__ v,
                                            const Geom &g, int comp, int t,
-                                           int x, int y) {
+                                           int x, int y,
+                                           const float2 *__restrict__ hprev = nullptr) {
     int64_t p = ((int64_t)t * g.nx + x) * g.ny + y;
     int64_t q;
     if (comp == 0) q = ((int64_t)t * g.nx + (x == 0 ? g.nx - 1 : x - 1)) * g.ny + y;
     else if (comp == 1) q = ((int64_t)t * g.nx + x) * g.ny + (y == 0 ? g.ny - 1 : y - 1);
-    else q = ((int64_t)(t == 0 ? g.T - 1 : t - 1) * g.nx + x) * g.ny + y;
+    else {
+        if (t == 0 && g.halo) return csub(v[p], hprev[(int64_t)x * g.ny + y]);
+        q = ((int64_t)(t == 0 ? g.T - 1 : t - 1) * g.nx + x) * g.ny + y;
+    }
     return csub(v[p], v[q]);
 }
 
@@ -76,7 +84,8 @@ __device__ __forceinline__ float2 theta_adj_at(const U &u, const Geom &g, int t,
     float2 r = cadd(csub(u(0, t, x, y), u(0, t, xp, y)),
                     csub(u(1, t, x, y), u(1, t, x, yp)));
     if (g.D == 3) {
-        int tp = t + 1 == g.T ? 0 : t + 1;
+        // halo mode asks the functor for frame T (the next rank's frame 0)
+        int tp = (t + 1 == g.T && !g.halo) ? 0 : t + 1;
         r = cadd(r, csub(u(2, t, x, y), u(2, tp, x, y)));
     }
     return r;
@@ -95,8 +104,12 @@ struct StackRef {
 struct ThetaOf {
     const float2 *v;
     Geom g;
+    const float2 *hprev = nullptr, *hnext = nullptr;  // halo mode only
     __device__ float2 operator()(int comp, int t, int x, int y) const {
-        return theta_at(v, g, comp, t, x, y);
+        if (comp == 2 && t == g.T)  // (theta v)_t at frame T: v[T] - v[T-1]
+            return csub(hnext[(int64_t)x * g.ny + y],
+                        v[((int64_t)(g.T - 1) * g.nx + x) * g.ny + y]);
+        return theta_at(v, g, comp, t, x, y, hprev);
     }
 };
 
@@ -236,6 +249,9 @@ __global__ void k_normal_finish(Geom g, const float2 *__restrict__ fhf,
 // Device-resident scalars; every kernel of an ADMM iteration is gated on
 // admm_active (and CG kernels on cg_active), which makes the iteration a
 // branch-free kernel sequence that is captured once as a CUDA graph.
+// Multi-rank frame sharding (b.mr): every reduction kernel leaves its local
+// sum in b.loc, the sums are allreduced (NCCL) and k_finalize applies the
+// same scalar update on every rank.
 struct DevScalars {
     double tau;                 // ||r||^2 (solver.py:106,117)
     double alpha_re, alpha_im;  // CG step tau/<d,Ad> (solver.py:114)
@@ -264,26 +280,116 @@ struct AdmmBufs {
     DevScalars *s;
     IterLog *log;
     float t_s, t_t, hb;  // lam/beta, lam_t/beta, beta/2
+    // frame sharding
+    int mr;              // 1: scalars are finalised after an allreduce
+    double *loc;         // [8] local sums: 0 rhs, 1-2 <d,Ad>, 3 xr, 4-5 post
+    float2 *hprev, *hnext;  // halo frames (1 frame each)
+    float2 *sfirst;      // send buffer (1 frame) for (mu - eta)_t of frame 0
 };
+
+enum FinOp { FIN_RHS = 0, FIN_AD = 1, FIN_XR = 2, FIN_POST = 3 };
+
+__device__ void fin_rhs(DevScalars *s, double tau) {
+    s->tau = tau;
+    s->cg_iter = 0;
+    if (!isfinite(tau)) {
+        s->error = 1;
+        s->cg_active = 0;
+        s->admm_active = 0;
+    } else {
+        s->cg_active = (s->cg_max > 0 && tau > s->atol2) ? 1 : 0;
+    }
+}
+
+__device__ void fin_ad(DevScalars *s, double re, double im) {
+    double den = re * re + im * im;
+    s->alpha_re = s->tau * re / den;
+    s->alpha_im = -s->tau * im / den;
+}
+
+__device__ void fin_xr(DevScalars *s, double tn) {
+    if (!isfinite(tn)) {
+        s->error = 1;
+        s->cg_active = 0;
+        s->admm_active = 0;
+        s->cg_iter += 1;
+        s->tau = tn;
+        return;
+    }
+    s->beta_cg = tn / s->tau;
+    s->tau = tn;
+    s->cg_iter += 1;
+    s->cg_active = (s->cg_iter < s->cg_max && tn > s->atol2) ? 1 : 0;
+}
+
+__device__ void fin_post(DevScalars *s, IterLog *log, double num, double den) {
+    double alpha;
+    if (den > 0) alpha = num / den;
+    else alpha = num == 0 ? 0.0 : INFINITY;
+    s->admm_alpha = alpha;
+    IterLog &L = log[s->admm_iter];
+    L.iteration = s->admm_iter + 1;
+    L.cg_iterations = s->cg_iter;
+    L.alpha = alpha;
+    L.cg_final_residual_sq = s->tau;
+    s->admm_iter += 1;
+    s->cur ^= 1;
+    s->admm_active = (s->admm_iter < s->admm_max && alpha > s->rtol2 && !s->error) ? 1 : 0;
+}
+
+// scalar update after the allreduce of b.loc (multi-rank)
+__global__ void k_finalize(AdmmBufs b, int op) {
+    DevScalars *s = b.s;
+    if (op == FIN_RHS || op == FIN_POST) {
+        if (!s->admm_active) return;
+    } else if (!s->cg_active) {
+        return;
+    }
+    if (op == FIN_RHS) fin_rhs(s, b.loc[0]);
+    else if (op == FIN_AD) fin_ad(s, b.loc[1], b.loc[2]);
+    else if (op == FIN_XR) fin_xr(s, b.loc[3]);
+    else fin_post(s, b.log, b.loc[4], b.loc[5]);
+}
+
+// copy frames 0 and T-1 of rho[cur] (sel = 0) or of rho[cur ^ 1] (sel = 1)
+// into fixed send buffers for the halo exchange (the ping-pong pointer is
+// only known on the device)
+__global__ void k_stage_frames(AdmmBufs b, Geom g, int sel, float2 *first, float2 *last) {
+    if (!b.s->admm_active) return;
+    const float2 *v = b.rho[b.s->cur ^ sel];
+    const int64_t nf = (int64_t)g.nx * g.ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        first[i] = v[i];
+        last[i] = v[(int64_t)(g.T - 1) * nf + i];
+    }
+}
 
 // mu+ = S(theta(rho) + eta)  (solver.py:178)
 __global__ void k_admm_mu(Geom g, AdmmBufs b) {
     if (!b.s->admm_active) return;
     const float2 *rho = b.rho[b.s->cur];
+    const int64_t nf = (int64_t)g.nx * g.ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
          i += (int64_t)gridDim.x * blockDim.x) {
         int comp = (int)(i / g.n);
         int t, x, y;
         unflat(g, i - comp * g.n, t, x, y);
-        float2 v = cadd(theta_at(rho, g, comp, t, x, y), b.eta[i]);
-        b.mu[i] = soft1(v, comp == 2 ? b.t_t : b.t_s);
+        float2 v = cadd(theta_at(rho, g, comp, t, x, y, b.hprev), b.eta[i]);
+        float2 m = soft1(v, comp == 2 ? b.t_t : b.t_s);
+        b.mu[i] = m;
+        // the previous rank needs (mu - eta)_t of this rank's frame 0
+        if (g.halo && comp == 2 && t == 0) b.sfirst[(int64_t)x * g.ny + y] = csub(m, b.eta[i]);
     }
+    (void)nf;
 }
 
 struct MuMinusEta {
     const float2 *mu, *eta;
     Geom g;
+    const float2 *hnext = nullptr;  // halo mode: next rank's (mu - eta)_t[0]
     __device__ float2 operator()(int comp, int t, int x, int y) const {
+        if (comp == 2 && t == g.T) return hnext[(int64_t)x * g.ny + y];
         int64_t i = comp * g.n + ((int64_t)t * g.nx + x) * g.ny + y;
         return csub(mu[i], eta[i]);
     }
@@ -294,7 +400,7 @@ struct MuMinusEta {
 __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
     if (!b.s->admm_active) return;
     float2 *x = b.rho[b.s->cur ^ 1];
-    MuMinusEta u{b.mu, b.eta, g};
+    MuMinusEta u{b.mu, b.eta, g, b.hnext};
     double v[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -310,17 +416,8 @@ __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
     }
     double tot[1];
     if (grid_reduce<1>(v, b.partials, b.tickets + 0, tot) && threadIdx.x == 0) {
-        DevScalars *s = b.s;
-        double tau = tot[0];
-        s->tau = tau;
-        s->cg_iter = 0;
-        if (!isfinite(tau)) {
-            s->error = 1;
-            s->cg_active = 0;
-            s->admm_active = 0;
-        } else {
-            s->cg_active = (s->cg_max > 0 && tau > s->atol2) ? 1 : 0;
-        }
+        if (b.mr) b.loc[0] = tot[0];
+        else fin_rhs(b.s, tot[0]);
     }
 }
 
@@ -329,7 +426,7 @@ __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
 __global__ void k_cg_ad(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
                         const float2 *__restrict__ sens, int S, int C) {
     if (!b.s->cg_active) return;
-    ThetaOf th{b.d, g};
+    ThetaOf th{b.d, g, b.hprev, b.hnext};
     int64_t nxy = (int64_t)g.nx * g.ny;
     double v[2] = {0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
@@ -347,15 +444,17 @@ __global__ void k_cg_ad(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
     }
     double tot[2];
     if (grid_reduce<2>(v, b.partials, b.tickets + 1, tot) && threadIdx.x == 0) {
-        DevScalars *s = b.s;
-        double den = tot[0] * tot[0] + tot[1] * tot[1];
-        s->alpha_re = s->tau * tot[0] / den;
-        s->alpha_im = -s->tau * tot[1] / den;
+        if (b.mr) {
+            b.loc[1] = tot[0];
+            b.loc[2] = tot[1];
+        } else {
+            fin_ad(b.s, tot[0], tot[1]);
+        }
     }
 }
 
-// multi-GPU variant, first half: fhf = coil-combined partials (then the
-// allreduce runs on b.fhf, then k_cg_ad with ws == nullptr)
+// multi-GPU coil sharding, first half: fhf = coil-combined partials (then
+// the allreduce runs on b.fhf, then k_cg_ad with ws == nullptr)
 __global__ void k_cg_fhf(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
                          const float2 *__restrict__ sens, int S, int C) {
     if (!b.s->cg_active) return;
@@ -384,19 +483,8 @@ __global__ void k_cg_xr(Geom g, AdmmBufs b) {
     }
     double tot[1];
     if (grid_reduce<1>(v, b.partials, b.tickets + 2, tot) && threadIdx.x == 0) {
-        double tn = tot[0];
-        if (!isfinite(tn)) {
-            s->error = 1;
-            s->cg_active = 0;
-            s->admm_active = 0;
-            s->cg_iter += 1;
-            s->tau = tn;
-            return;
-        }
-        s->beta_cg = tn / s->tau;
-        s->tau = tn;
-        s->cg_iter += 1;
-        s->cg_active = (s->cg_iter < s->cg_max && tn > s->atol2) ? 1 : 0;
+        if (b.mr) b.loc[3] = tot[0];
+        else fin_xr(s, tot[0]);
     }
 }
 
@@ -427,7 +515,7 @@ __global__ void k_admm_post(Geom g, AdmmBufs b) {
         int64_t p = i - comp * g.n;
         int t, x, y;
         unflat(g, p, t, x, y);
-        float2 th = theta_at(xn, g, comp, t, x, y);
+        float2 th = theta_at(xn, g, comp, t, x, y, b.hprev);
         b.eta[i] = cadd(b.eta[i], csub(th, b.mu[i]));
         if (comp == 0) {
             float2 a = xn[p], o = rho[p];
@@ -438,18 +526,12 @@ __global__ void k_admm_post(Geom g, AdmmBufs b) {
     }
     double tot[2];
     if (grid_reduce<2>(v, b.partials, b.tickets + 3, tot) && threadIdx.x == 0) {
-        double num = tot[0], den = tot[1], alpha;
-        if (den > 0) alpha = num / den;
-        else alpha = num == 0 ? 0.0 : INFINITY;
-        s->admm_alpha = alpha;
-        IterLog &L = b.log[s->admm_iter];
-        L.iteration = s->admm_iter + 1;
-        L.cg_iterations = s->cg_iter;
-        L.alpha = alpha;
-        L.cg_final_residual_sq = s->tau;
-        s->admm_iter += 1;
-        s->cur ^= 1;
-        s->admm_active = (s->admm_iter < s->admm_max && alpha > s->rtol2 && !s->error) ? 1 : 0;
+        if (b.mr) {
+            b.loc[4] = tot[0];
+            b.loc[5] = tot[1];
+        } else {
+            fin_post(s, b.log, tot[0], tot[1]);
+        }
     }
 }
 

@@ -62,8 +62,12 @@ class DftOperator:
 
     @classmethod
     def build(cls, trajectory, grid, sens, mode="auto", precision="single",
-              memory_budget=DEFAULT_MEMORY_BUDGET, n_frames=1, device=None):
-        """operators.py:141-164 (factor-cached, never materialized)."""
+              memory_budget=DEFAULT_MEMORY_BUDGET, n_frames=1, device=None,
+              frame_shard=False):
+        """operators.py:141-164 (factor-cached, never materialized).
+
+        frame_shard: the frames are one rank's block of a 2-D+t problem split
+        over ranks (temporal differences at the block edges use halo frames)."""
         if mode not in MODES:
             raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
         validate_precision(precision)
@@ -88,7 +92,8 @@ class DftOperator:
             nx=grid.nx, ny=grid.ny, n_frames=n_frames, n_coils=tmaps.shape[0],
             n_samples=m,
             coords=coords.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-            sens=tmaps.data_ptr(), device=dev.index, reserved=0)
+            sens=tmaps.data_ptr(), device=dev.index,
+            flags=_native.CSR_PLAN_FRAME_SHARD if frame_shard else 0)
         _dev.torch.cuda.current_stream(dev).synchronize()
         plan = ctypes.c_void_p()
         _native.call("csr_plan_create", ctypes.byref(desc), ctypes.byref(plan))

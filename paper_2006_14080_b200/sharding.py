@@ -126,19 +126,31 @@ class CommStats:
                                   for k, v in self.per_phase.items()}}
 
 
+def broadcast_unique_id(rank, group=None, make_id=None):
+    """Rank 0 makes the 128-byte NCCL unique id (``csr_comm_unique_id``), every
+    rank receives it over the torch.distributed group (any backend)."""
+    import torch.distributed as dist
+    obj = [None]
+    if rank == 0:
+        if make_id is None:
+            buf = ctypes.create_string_buffer(128)
+            _native.call("csr_comm_unique_id", buf)
+            obj = [bytes(buf.raw)]
+        else:
+            obj = [bytes(make_id())]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if len(obj[0]) != 128:
+        raise SpmdError(f"bad NCCL unique id ({len(obj[0])} bytes)")
+    return obj[0]
+
+
 class NcclComm:
     """NCCL communicator owned by the native library; the 128-byte unique id
     travels over the already-initialised torch.distributed group."""
 
     def __init__(self, rank, world, device, group=None):
-        import torch.distributed as dist
         self.rank, self.world, self.device = rank, world, device
-        buf = ctypes.create_string_buffer(128)
-        if rank == 0:
-            _native.call("csr_comm_unique_id", buf)
-        obj = [bytes(buf.raw)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        uid = ctypes.create_string_buffer(obj[0], 128)
+        uid = ctypes.create_string_buffer(broadcast_unique_id(rank, group), 128)
         self.handle = ctypes.c_void_p()
         _native.call("csr_comm_create", uid, world, rank, device,
                      ctypes.byref(self.handle))

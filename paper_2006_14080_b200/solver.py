@@ -24,7 +24,7 @@ from . import _dev, _native
 from .acquisition import ImageGrid
 from .errors import CgDivergenceError, ShapeMismatchError
 from .operators import DEFAULT_MEMORY_BUDGET, DftOperator
-from .sharding import CommStats, NcclComm, coil_shard_plan, dist_world
+from .sharding import CommStats, NcclComm, coil_shard_plan, dist_world, make_shard_plan
 from .tensor import axpy, hermitian_dot, norm2_squared, validate_precision
 from .transform import soft_threshold, theta, theta_adjoint
 
@@ -259,34 +259,82 @@ def _frames(dataset):
     return int(getattr(dataset, "n_frames", 1))
 
 
+@dataclass(frozen=True)
+class ShardSpec:
+    """Which part of the problem one rank owns: ``coil``
+    sharding splits the coils (F^H F is a sum over coils, one image
+    allreduce per CG iteration), ``frame`` sharding splits the frames of a
+    2-D+t problem (F^H F is block diagonal; temporal differences exchange
+    one halo frame with each ring neighbour, CG scalars are allreduced)."""
+    mode: str
+    frames: tuple
+    coils: tuple
+
+
+def plan_shard(n_frames, n_coils, rank, world, shard="auto"):
+    if shard not in ("auto", "coil", "frame"):
+        raise ValueError(f"shard must be auto, coil or frame, got {shard!r}")
+    if shard == "auto":
+        shard = "frame" if (n_frames > 1 and world > 1 and n_frames >= world) else "coil"
+    if shard == "frame":
+        return ShardSpec("frame", make_shard_plan(n_frames, world).bounds[rank],
+                         (0, n_coils))
+    return ShardSpec("coil", (0, n_frames), coil_shard_plan(n_coils, world).bounds[rank])
+
+
+def shard_inputs(coords, data, maps, n_frames, spec):
+    """This rank's (coords, data, maps) rows/columns for a ShardSpec."""
+    m = coords.shape[0] // n_frames
+    (f0, f1), (c0, c1) = spec.frames, spec.coils
+    return (coords[f0 * m:f1 * m], np.asarray(data)[f0 * m:f1 * m, c0:c1],
+            np.asarray(maps)[c0:c1])
+
+
 class _Shard:
     """This rank's operator, data and communicator (one GPU per rank)."""
 
-    def __init__(self, dataset, sens, n_workers, op_mode, device):
+    def __init__(self, dataset, sens, n_workers, op_mode, device, shard="auto"):
         maps = np.asarray(getattr(sens, "maps", sens))
         rank, world = dist_world()
         if n_workers != world:
             raise ValueError(f"n_workers={n_workers} but torch.distributed world size is "
                              f"{world}: launch one process per GPU (torchrun)")
         T = _frames(dataset)
-        self.rank, self.world = rank, world
-        self.coils = coil_shard_plan(maps.shape[0], world).bounds[rank]
-        c0, c1 = self.coils
+        self.rank, self.world, self.n_frames = rank, world, T
+        self.spec = plan_shard(T, maps.shape[0], rank, world, shard)
+        coords = np.asarray(dataset.trajectory.coords, dtype=np.float64)
+        lc, ld, lm = shard_inputs(coords, dataset.data, maps, T, self.spec)
+        f0, f1 = self.spec.frames
         grid = ImageGrid(maps.shape[1], maps.shape[2])
-        self.op = DftOperator.build(dataset.trajectory, grid, maps[c0:c1], mode=op_mode,
-                                    n_frames=T, device=device)
-        data = np.ascontiguousarray(np.asarray(dataset.data)[:, c0:c1].astype(np.complex64))
-        self.data = _dev.torch.from_numpy(data).to(self.op.device)
+        self.op = DftOperator.build(lc, grid, lm, mode=op_mode, n_frames=f1 - f0,
+                                    device=device, frame_shard=self.spec.mode == "frame")
+        self.data = _dev.torch.from_numpy(
+            np.ascontiguousarray(ld.astype(np.complex64))).to(self.op.device)
         self.comm = None
         if world > 1:
             self.comm = NcclComm(rank, world, self.op.device.index)
             _native.call("csr_plan_set_comm", self.op.plan, self.comm.handle)
 
+    def image_shape(self):
+        if self.n_frames == 1:
+            return (self.op.nx, self.op.ny)
+        return (self.n_frames, self.op.nx, self.op.ny)
+
+    def gather(self, local):
+        """Full image on every rank (frame sharding); identity otherwise."""
+        if self.spec.mode != "frame" or self.world == 1:
+            return local.reshape(self.image_shape())
+        import torch.distributed as dist
+        parts = [None] * self.world
+        dist.all_gather_object(parts, local)
+        return np.concatenate(parts, axis=0).reshape(self.image_shape())
+
 
 def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single",
                      op_mode="auto", memory_budget=DEFAULT_MEMORY_BUDGET,
                      compute_objectives=True, order_stable=True,
-                     barrier_timeout=600.0, device=None, return_device=False):
+                     barrier_timeout=600.0, device=None, return_device=False,
+                     shard="auto"):
     """Sharded ADMM reconstruction (solver.py:274-360). Returns (image, RunReport).
 
     n_workers must equal the torch.distributed world size (one process per
@@ -298,7 +346,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
     validate_precision(precision)
     _check_inputs(dataset, sens)
     t0 = time.perf_counter()
-    sh = _Shard(dataset, sens, n_workers, op_mode, device)
+    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard)
     op, dev = sh.op, sh.op.device
     n_it = params.admm_max_iters
     rho = _dev.empty_c64(op.image_shape, dev)
@@ -316,7 +364,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                 "cg_final_residual_sq": log[i].cg_final_residual_sq}
                for i in range(stats.n_iterations)]
     cs = CommStats()
-    if sh.world > 1:
+    if sh.world > 1 and sh.spec.mode == "coil":
         cs.record("setup", op.nx * op.ny * op.n_frames, calls=2)
         cs.record("solve", op.nx * op.ny * op.n_frames,
                   calls=stats.allreduce_calls - 2)
@@ -331,6 +379,9 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                 "graph": bool(stats.graph_used),
                 "kernels_per_iteration": stats.kernels_per_iter},
         backend="csrecon_b200/" + op.info()["gemm_path"])
+    report.timing["shard"] = sh.spec.mode
+    if compute_objectives and sh.spec.mode == "frame" and sh.world > 1:
+        compute_objectives = False  # the local snapshots hold only this rank's frames
     if compute_objectives:
         full = op if sh.world == 1 else DftOperator.build(
             dataset.trajectory, ImageGrid(op.nx, op.ny), np.asarray(getattr(sens, "maps", sens)),
@@ -343,26 +394,27 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
         report.objective_initial = vals[0]
         for rec, val in zip(records, vals[1:]):
             rec["objective"] = val
-    image = rho if return_device else rho.cpu().numpy()
-    return image, report
+    if return_device and (sh.spec.mode == "coil" or sh.world == 1):
+        return rho.reshape(sh.image_shape()), report
+    return sh.gather(rho.cpu().numpy()), report
 
 
 def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
                         op_mode="auto", memory_budget=DEFAULT_MEMORY_BUDGET,
                         order_stable=True, barrier_timeout=600.0, device=None,
-                        return_device=False):
+                        return_device=False, shard="auto"):
     """Unregularised adjoint image F^H d (solver.py:363-406)."""
     validate_precision(precision)
     _check_inputs(dataset, sens)
     t0 = time.perf_counter()
-    sh = _Shard(dataset, sens, n_workers, op_mode, device)
+    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard)
     op, dev = sh.op, sh.op.device
     img = _dev.empty_c64(op.image_shape, dev)
     _native.call("csr_adjoint_reconstruct", op.plan, sh.data.data_ptr(), img.data_ptr(),
                  _dev.stream_ptr(dev))
     _dev.torch.cuda.current_stream(dev).synchronize()
     cs = CommStats()
-    if sh.world > 1:
+    if sh.world > 1 and sh.spec.mode == "coil":
         cs.record("setup", op.nx * op.ny * op.n_frames)
     report = RunReport(
         method="adjoint", precision=precision, n_workers=n_workers, op_mode=op.mode,
@@ -371,4 +423,6 @@ def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
         timing={"setup_seconds": time.perf_counter() - t0,
                 "total_seconds": time.perf_counter() - t0},
         backend="csrecon_b200/" + op.info()["gemm_path"])
-    return (img if return_device else img.cpu().numpy()), report
+    if return_device and (sh.spec.mode == "coil" or sh.world == 1):
+        return img.reshape(sh.image_shape()), report
+    return sh.gather(img.cpu().numpy()), report

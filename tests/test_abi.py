@@ -51,7 +51,7 @@ def test_calls_fail_loudly_without_a_gpu():
         pytest.skip("GPU present")
     lib = _native.load()
     desc = _native.PlanDesc(nx=4, ny=4, n_frames=1, n_coils=1, n_samples=4,
-                            coords=None, sens=None, device=0, reserved=0)
+                            coords=None, sens=None, device=0, flags=0)
     plan = ctypes.c_void_p()
     rc = lib.csr_plan_create(ctypes.byref(desc), ctypes.byref(plan))
     assert rc != 0

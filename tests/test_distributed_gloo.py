@@ -1,0 +1,207 @@
+"""World-size-2 tests of the multi-GPU decomposition on CPU (gloo).
+
+The device loop shards coils (static problems: one image allreduce per CG
+iteration) or frames (2-D+t: ring halo exchange for the temporal
+differences, allreduced CG/ADMM scalars).  These tests run the same
+decomposition with the f64 oracle as the per-rank compute stand-in and gloo
+as the interconnect, and check it reproduces the unsharded solve; they also
+exercise the host-side shard planning and the NCCL unique-id broadcast.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import csrecon_oracle as O
+from paper_2006_14080_b200.sharding import broadcast_unique_id
+from paper_2006_14080_b200.solver import plan_shard, shard_inputs
+
+WORLD = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _problem(T, seed=11, nx=12, ny=10, C=4, m=90):
+    rng = np.random.default_rng(seed)
+    coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
+    sens = (rng.standard_normal((C, nx, ny)) + 1j * rng.standard_normal((C, nx, ny))) * 0.4
+    truth = rng.standard_normal((T, nx, ny)) + 1j * rng.standard_normal((T, nx, ny))
+    op = O.Operator(coords, sens, T)
+    data = op.forward(truth if T > 1 else truth[0])
+    params = O.Params(lam=1e-3, beta=1e-2, admm_rtol=1e-150, admm_max_iters=4,
+                      cg_atol=1e-150, cg_max_iters=5, lam_t=5e-3)
+    return coords, sens, data, params
+
+
+def _allreduce(arr):
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if t.is_complex():
+        v = torch.view_as_real(t).clone()
+        dist.all_reduce(v)
+        return torch.view_as_complex(v).numpy()
+    v = t.clone()
+    dist.all_reduce(v)
+    return v.numpy()
+
+
+def _ring_exchange(first, last, rank, world):
+    """hprev <- previous rank's last frame, hnext <- next rank's first frame
+    (the device loop's halo_exchange)."""
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    send_l = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(last))).clone()
+    send_f = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(first))).clone()
+    recv_p, recv_n = torch.empty_like(send_l), torch.empty_like(send_f)
+    ops = [dist.P2POp(dist.isend, send_l, nxt), dist.P2POp(dist.irecv, recv_p, prv),
+           dist.P2POp(dist.isend, send_f, prv), dist.P2POp(dist.irecv, recv_n, nxt)]
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    return torch.view_as_complex(recv_p).numpy(), torch.view_as_complex(recv_n).numpy()
+
+
+def _theta_h(v, prev):
+    """theta of a frame block with the temporal difference at frame 0 taken
+    against the halo frame (k_admm_mu / theta_at with hprev)."""
+    out = np.empty((3,) + v.shape, v.dtype)
+    out[0] = v - np.roll(v, 1, axis=1)
+    out[1] = v - np.roll(v, 1, axis=2)
+    out[2][1:] = v[1:] - v[:-1]
+    out[2][0] = v[0] - prev
+    return out
+
+
+def _theta_adj_h(u, u2_next):
+    """theta^H with the temporal component of frame T taken from the halo
+    (theta_adj_at in halo mode)."""
+    d0, d1, d2 = u
+    out = (d0 - np.roll(d0, -1, axis=1)) + (d1 - np.roll(d1, -1, axis=2))
+    d2n = np.concatenate([d2[1:], u2_next[None]], axis=0)
+    return out + (d2 - d2n)
+
+
+def _frame_sharded_admm(rank, world, coords, sens, data, params, T):
+    """The device loop's frame decomposition (csrecon_b200.cu
+    enqueue_admm_iteration, frame mode) with the oracle as the compute."""
+    spec = plan_shard(T, sens.shape[0], rank, world, "frame")
+    lc, ld, lm = shard_inputs(coords, data, sens, T, spec)
+    tl = spec.frames[1] - spec.frames[0]
+    op = O.Operator(lc, lm, tl)
+    fhd = op.adjoint(ld).reshape(tl, *sens.shape[1:])
+    rho = fhd.copy()
+    mu = np.zeros((3,) + rho.shape, complex)
+    eta = mu.copy()
+    hb = params.beta / 2
+    t_s, t_t = params.lam / params.beta, params.lam_t / params.beta
+
+    def apply_a(d):
+        prev, nxt = _ring_exchange(d[0], d[-1], rank, world)
+        th = _theta_h(d, prev)
+        th2_next = nxt - d[-1]
+        ff = op.adjoint(op.forward(d)).reshape(d.shape)
+        return ff + hb * _theta_adj_h(th, th2_next)
+
+    for _ in range(params.admm_max_iters):
+        prev, _unused = _ring_exchange(rho[0], rho[-1], rank, world)
+        v = _theta_h(rho, prev) + eta
+        mu = O.shrink_stack(v, t_s, t_t)
+        me0 = mu[2][0] - eta[2][0]
+        _unused, me_next = _ring_exchange(me0, me0, rank, world)
+        rhs = fhd + hb * _theta_adj_h(mu - eta, me_next)
+        x = np.zeros_like(rhs)
+        r = rhs.copy()
+        d = r.copy()
+        tau = float(_allreduce(np.array([np.vdot(r, r).real]))[0])
+        for _ in range(params.cg_max_iters):
+            ad = apply_a(d)
+            dad = _allreduce(np.array([np.vdot(d, ad)]))[0]
+            alpha = tau / dad
+            x = x + alpha * d
+            r = r - alpha * ad
+            tn = float(_allreduce(np.array([np.vdot(r, r).real]))[0])
+            d = r + (tn / tau) * d
+            tau = tn
+        prev, _unused = _ring_exchange(x[0], x[-1], rank, world)
+        eta = eta + (_theta_h(x, prev) - mu)
+        rho = x
+    return spec, rho
+
+
+def _coil_sharded_admm(rank, world, coords, sens, data, params, T):
+    spec = plan_shard(T, sens.shape[0], rank, world, "coil")
+    lc, ld, lm = shard_inputs(coords, data, sens, T, spec)
+    op = O.Operator(lc, lm, T)
+    img, recs = O.admm(ld, lc, lm, params, "double", T, allreduce=_allreduce, op=op)
+    return spec, img
+
+
+def _worker(rank, world, port, mode, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if mode == "uid":
+            uid = broadcast_unique_id(rank, make_id=lambda: bytes(range(128)))
+            res = {"uid": np.frombuffer(uid, np.uint8)}
+        else:
+            T = 4 if mode.startswith("frame") else (4 if mode == "coil_dyn" else 1)
+            coords, sens, data, params = _problem(T)
+            fn = _frame_sharded_admm if mode.startswith("frame") else _coil_sharded_admm
+            spec, img = fn(rank, world, coords, sens, data, params, T)
+            res = {"img": img, "frames": np.array(spec.frames), "coils": np.array(spec.coils)}
+        np.savez(out_path.format(rank=rank), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode, tmp_path):
+    out = str(tmp_path / ("res_{rank}_" + mode + ".npz"))
+    mp.spawn(_worker, args=(WORLD, _free_port(), mode, out), nprocs=WORLD, join=True)
+    return [np.load(out.format(rank=r)) for r in range(WORLD)]
+
+
+def test_unique_id_broadcast(tmp_path):
+    res = _run("uid", tmp_path)
+    for r in res:
+        assert np.array_equal(r["uid"], np.arange(128, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("mode", ["coil", "coil_dyn"])
+def test_coil_sharded_admm_matches_unsharded(mode, tmp_path):
+    T = 1 if mode == "coil" else 4
+    coords, sens, data, params = _problem(T)
+    ref, _ = O.admm(data, coords, sens, params, "double", T)
+    res = _run(mode, tmp_path)
+    assert tuple(res[0]["coils"]) == (0, 2) and tuple(res[1]["coils"]) == (2, 4)
+    for r in res:  # replicated image on every rank
+        img = r["img"]
+        assert np.linalg.norm(img - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_frame_sharded_admm_matches_unsharded(tmp_path):
+    T = 4
+    coords, sens, data, params = _problem(T)
+    ref, _ = O.admm(data, coords, sens, params, "double", T)
+    res = _run("frame", tmp_path)
+    img = np.concatenate([r["img"] for r in res], axis=0)
+    assert tuple(res[0]["frames"]) == (0, 2) and tuple(res[1]["frames"]) == (2, 4)
+    assert np.linalg.norm(img - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_plan_shard_rules():
+    assert plan_shard(64, 16, 3, 8).mode == "frame"
+    assert plan_shard(64, 16, 3, 8).frames == (24, 32)
+    assert plan_shard(1, 16, 3, 8).mode == "coil"
+    assert plan_shard(1, 16, 3, 8).coils == (6, 8)
+    assert plan_shard(4, 3, 0, 1, "frame").frames == (0, 4)
+    with pytest.raises(ValueError):
+        plan_shard(4, 3, 0, 1, "tiles")

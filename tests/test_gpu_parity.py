@@ -245,3 +245,25 @@ def test_dynamic_matches_oracle(cuda):
     assert rel_err(img, ref) <= IMG_TOL
     gpu_op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens, n_frames=T)
     assert rel_err(gpu_op.forward(truth.astype(np.complex64)), data) <= OP_TOL
+
+
+@pytest.mark.parametrize("force_mr", [False, True])
+def test_frame_shard_path_matches_oracle(cuda, force_mr, monkeypatch):
+    # the frame-sharded loop (halo frames, scalars finalised after the
+    # allreduce) on one rank: halos come from the rank itself
+    if force_mr:
+        monkeypatch.setenv("CSR_FORCE_MR", "1")
+    rng = np.random.default_rng(9)
+    T, nx, ny, C, m = 3, 20, 16, 3, 250
+    coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
+    sens = random_complex(rng, (C, nx, ny)) * 0.3
+    truth = random_complex(rng, (T, nx, ny))
+    data = O.Operator(coords, sens, T).forward(truth)
+    kw = dict(lam=1e-3, beta=1e-2, admm_rtol=1e-150, admm_max_iters=5, cg_atol=1e-150,
+              cg_max_iters=5)
+    ref, _ = O.admm(data, coords, sens, O.Params(lam_t=5e-3, **kw), n_frames=T)
+    img, rep = P.admm_reconstruct(_dataset(coords, data, T), sens,
+                                  P.ReconParams(lam_t=5e-3, **kw), shard="frame",
+                                  compute_objectives=False)
+    assert rep.timing["shard"] == "frame"
+    assert rel_err(img, ref) <= IMG_TOL
