@@ -84,6 +84,50 @@ __device__ bool grid_reduce(double (&v)[NV], double *partials,
     return true;
 }
 
+// exact power of two s with s * bound <= 2^14 (1 for bound == 0)
+__device__ __forceinline__ float pow2_scale(float bound) {
+    if (!(bound > 0.f) || !isfinite(bound)) return 1.f;
+    int e;
+    frexpf(bound, &e);  // bound = m * 2^e, m in [0.5, 1)
+    int s = 14 - e;
+    s = max(-120, min(120, s));
+    return ldexpf(1.f, s);
+}
+
+// deterministic grid max of non-negative values: true in thread 0 of the
+// last block to finish, with the maximum in `out`
+__device__ bool grid_max(float v, double *partials, unsigned *ticket, float &out) {
+    __shared__ float sh[32];
+    __shared__ int last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        float w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+        if (lane == 0) partials[blockIdx.x] = w;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    if (warp != 0) return false;
+    float w = 0.f;
+    for (unsigned b = lane; b < gridDim.x; b += 32) w = fmaxf(w, (float)__ldcg(partials + b));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+    if (lane != 0) return false;
+    *ticket = 0u;
+    out = w;
+    return true;
+}
+
 // Plan buffers come from the device's default stream-ordered pool with an
 // unbounded release threshold, so building and dropping plans (one per
 // reconstruction call) reuses memory instead of paying cudaMalloc/cudaFree

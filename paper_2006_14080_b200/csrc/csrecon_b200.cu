@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -96,6 +97,7 @@ struct csr_plan {
     bool frame_mode = false;
     float2 *hprev = nullptr, *hnext = nullptr, *sfirst = nullptr, *slast = nullptr;
     double *loc = nullptr;
+    double *mpart = nullptr;  // grid-max partials of the d producers
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
     int64_t flush_bytes = 0;
@@ -145,10 +147,12 @@ int check_device(int dev) {
 // in the plan's internal k-space buffer (what run_adjoint_partials(nullptr)
 // consumes); otherwise it is written as (T*M, C).
 int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
-                const int *gate) {
+                const int *gate, bool in_loop = false) {
     if (p->tc.enabled) {
-        if (tc_forward(p->tc, x, out, st, gate)) return fail(CSR_ERR_CUDA, "tc forward launch");
-        g_launches.fetch_add(p->tc.fwd_launches, std::memory_order_relaxed);
+        if (tc_forward(p->tc, x, out, st, gate, in_loop))
+            return fail(CSR_ERR_CUDA, "tc forward launch");
+        g_launches.fetch_add(tc_forward_launches(p->tc, in_loop, out != nullptr),
+                             std::memory_order_relaxed);
         return CSR_OK;
     }
     dim3 grid((unsigned)((p->M + ST - 1) / ST), (unsigned)p->C, (unsigned)p->T);
@@ -264,6 +268,9 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
     b.hprev = p->hprev;
     b.hnext = p->hnext;
     b.sfirst = p->sfirst;
+    b.tcs = p->tc.enabled ? p->tc.scales : nullptr;
+    b.mpart = p->mpart;
+    b.mtick = p->tickets + 4;
     return b;
 }
 
@@ -288,8 +295,8 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     const int64_t nf = (int64_t)g.nx * g.ny;
     for (int it = 0; it < cg_max; ++it) {
         if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
-        TRY(run_forward(p, p->d, nullptr, st, gate));
-        k += p->tc.enabled ? p->tc.fwd_launches : 1;
+        TRY(run_forward(p, p->d, nullptr, st, gate, true));
+        k += p->tc.enabled ? tc_forward_launches(p->tc, true, false) : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.adj_launches : 1;
         if (coil_multi) {
@@ -429,6 +436,7 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     if ((rc = dalloc(p, &p->ad, (size_t)n, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->partials, (size_t)(4 * 148 * 4), &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->loc, 8, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->mpart, (size_t)(4 * 148), &p->ws_bytes))) return cleanup(rc);
     if (p->frame_mode) {
         if ((rc = dalloc(p, &p->hprev, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
         if ((rc = dalloc(p, &p->hnext, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
@@ -754,6 +762,13 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
 }
 
 // ---- NCCL ---------------------------------------------------------------
+// debug: copy the tensor-core trace buffer (CSR_TRACE) to the host
+int csr_debug_trace(csr_plan *p, unsigned long long *host, int64_t n) {
+    if (!p || !p->tc.trace) return fail(CSR_ERR_ARG, "no trace buffer (set CSR_TRACE)");
+    CU(cudaMemcpy(host, p->tc.trace, std::min<int64_t>(n, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
+    return CSR_OK;
+}
+
 int csr_plan_set_timing(csr_plan *p, void *flush_buf, int64_t flush_bytes,
                         float *iter_ms) {
     if (!p) return fail(CSR_ERR_ARG, "null plan");

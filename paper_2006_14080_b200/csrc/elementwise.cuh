@@ -285,6 +285,11 @@ struct AdmmBufs {
     double *loc;         // [8] local sums: 0 rhs, 1-2 <d,Ad>, 3 xr, 4-5 post
     float2 *hprev, *hnext;  // halo frames (1 frame each)
     float2 *sfirst;      // send buffer (1 frame) for (mu - eta)_t of frame 0
+    // tensor-core operand scaling: the producers of d (k_admm_rhs, k_cg_d)
+    // leave max|d| (component-wise) in tcs[6] for the next forward
+    float *tcs;
+    double *mpart;
+    unsigned *mtick;
 };
 
 enum FinOp { FIN_RHS = 0, FIN_AD = 1, FIN_XR = 2, FIN_POST = 3 };
@@ -402,6 +407,7 @@ __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
     float2 *x = b.rho[b.s->cur ^ 1];
     MuMinusEta u{b.mu, b.eta, g, b.hnext};
     double v[1] = {0.0};
+    float dmax = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int t, xx, y;
@@ -413,11 +419,16 @@ __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
         b.r[i] = rhs;
         b.d[i] = rhs;
         v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
+        dmax = fmaxf(dmax, fmaxf(fabsf(rhs.x), fabsf(rhs.y)));
     }
     double tot[1];
     if (grid_reduce<1>(v, b.partials, b.tickets + 0, tot) && threadIdx.x == 0) {
         if (b.mr) b.loc[0] = tot[0];
         else fin_rhs(b.s, tot[0]);
+    }
+    if (b.tcs) {
+        float m;
+        if (grid_max(dmax, b.mpart, b.mtick, m)) b.tcs[6] = m;
     }
 }
 
@@ -488,15 +499,22 @@ __global__ void k_cg_xr(Geom g, AdmmBufs b) {
     }
 }
 
-// d = r + (tau'/tau) d
+// d = r + (tau'/tau) d ; max|d| for the next forward's operand scale
 __global__ void k_cg_d(Geom g, AdmmBufs b) {
     DevScalars *s = b.s;
     if (!s->cg_active) return;
     float be = (float)s->beta_cg;
+    float dmax = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float2 d = b.d[i], r = b.r[i];
-        b.d[i] = make_float2(r.x + be * d.x, r.y + be * d.y);
+        float2 nd = make_float2(r.x + be * d.x, r.y + be * d.y);
+        b.d[i] = nd;
+        dmax = fmaxf(dmax, fmaxf(fabsf(nd.x), fabsf(nd.y)));
+    }
+    if (b.tcs) {
+        float m;
+        if (grid_max(dmax, b.mpart, b.mtick, m)) b.tcs[6] = m;
     }
 }
 

@@ -52,16 +52,21 @@ struct TcPlan {
     int64_t M = 0, Mk = 0;
     int Cp = 4, xs = 32, nxp = 0, nyp = 0, nyA = 0, Kf = 0, Nf = 0;
     int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
+    bool fwd_ts = false;  // A-stationary forward (2*nyp <= 256)
+    unsigned long long *trace = nullptr;  // CSR_TRACE: per-CTA timestamps
+    int G_ts = 1, ntpg_ts = 1, fts_smem = 0;
     int raw_bytes = 0, adj_stage = 0, fwd_smem = 0, adj_smem = 0, adj_cs = 1;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
     float2 *p0p = nullptr, *kdp = nullptr, *kdi = nullptr;
     const float2 *sens = nullptr;
-    float *scales = nullptr;  // [0]=sig_x [1]=1/sig_x [2]=sig_d [3]=1/sig_d [4]=max|s|
+    float *scales = nullptr;  // [4] max|s|, [5] max|kd|, [6] max|img| (component-wise);
+                              // operand scales are pow2_scale() of these bounds
     double *red = nullptr;
     unsigned *tick = nullptr;
     CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
+    CUtensorMap tm_xb128_hi, tm_xb128_lo;
 };
 
 // ---------------------------------------------------------------------------
@@ -75,60 +80,6 @@ __device__ __forceinline__ uint32_t pack2(__half a, __half b) {
 }
 __device__ __forceinline__ __half hneg(__half a) {
     return __ushort_as_half(__half_as_ushort(a) ^ 0x8000u);
-}
-// exact power of two s with s * bound <= 2^14 (1 for bound == 0)
-__device__ __forceinline__ float pow2_scale(float bound) {
-    if (!(bound > 0.f) || !isfinite(bound)) return 1.f;
-    int e;
-    frexpf(bound, &e);  // bound = m * 2^e, m in [0.5, 1)
-    int s = 14 - e;
-    s = max(-120, min(120, s));
-    return ldexpf(1.f, s);
-}
-
-// deterministic grid max of non-negative values: true in thread 0 of the
-// last block to finish, with the maximum in `out`
-__device__ bool grid_max(float v, double *partials, unsigned *ticket, float &out) {
-    __shared__ float sh[32];
-    __shared__ int last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    if (warp == 0) {
-        float w = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
-        if (lane == 0) partials[blockIdx.x] = w;
-    }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return false;
-    __threadfence();
-    if (warp != 0) return false;
-    float w = 0.f;
-    for (unsigned b = lane; b < gridDim.x; b += 32) w = fmaxf(w, (float)__ldcg(partials + b));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
-    if (lane != 0) return false;
-    *ticket = 0u;
-    out = w;
-    return true;
-}
-
-// scale pair (s, 1/s) for the operand bound factor * max
-__device__ void grid_max_scale(float v, double *partials, unsigned *ticket, float factor,
-                               float *out_scale) {
-    float m;
-    if (grid_max(v, partials, ticket, m)) {
-        const float s = pow2_scale(factor * m);
-        out_scale[0] = s;
-        out_scale[1] = 1.f / s;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -208,15 +159,18 @@ __global__ void k_tc_absmax_img(const float2 *__restrict__ img, int64_t n, doubl
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         v = fmaxf(v, fmaxf(fabsf(img[i].x), fabsf(img[i].y)));
-    grid_max_scale(v, partials, ticket, 2.f * scales[4], scales + 0);
+    float m;
+    if (grid_max(v, partials, ticket, m)) scales[6] = m;
 }
 
 // X' = split(sigma_x * s_c * img_t) laid out as doubled rows (x, c, part)
 __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
-                            const float2 *__restrict__ sens, const float *__restrict__ scales,
+                            const float2 *__restrict__ sens, float *scales,
                             __half *hi, __half *lo, const int *gate) {
     if (gate && !*gate) return;
-    const float sg = scales[0];
+    // exact power-of-two scale: |s_c * img| <= 2 max|s| max|img| (component-wise)
+    const float sg = pow2_scale(2.f * scales[4] * scales[6]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) scales[5] = 0.f;  // k-space max (atomicMax)
     const int hy = a.Kf / 2;  // complex y per row (nyp)
     int64_t total = (int64_t)a.T * a.nxp * a.Cp * hy;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -251,6 +205,7 @@ __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
 struct FwdParams {
     TcArgs a;
     int mt_per_frame, nt_per_group;
+    int amax;  // 1: kdp aliases the k-space buffer; atomicMax |kd| into scales[5]
     const float2 *p0p;
     float2 *kdp;  // [G][T][Mk][Cp]
     const float *scales;
@@ -404,8 +359,253 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[ab]);
         }
+        if (P.amax) {  // max|kd| for the adjoint's operand scale (order-free)
+            float mx = 0.f;
+            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+                mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(const_cast<float *>(P.scales) + 5),
+                                     __float_as_uint(mx));
+        }
         if (valid) {
-            const float inv = P.scales[1];
+            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
+            float2 *out = P.kdp + (((int64_t)blockIdx.y * P.a.T + t) * P.a.Mk + kloc) * CP;
+#pragma unroll
+            for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// Forward, A-stationary form (2*nyp <= 256).  Each CTA owns 128 samples of
+// one frame: their P1 rows (A, fp16 hi/lo) are loaded once into TMEM and
+// stay there while the image operand X' (B, 128 doubled rows = 64 complex
+// (x, c) columns per tile) streams through a 6-deep TMA ring; MMAs read A
+// from TMEM and only B from shared memory.  Double-buffered accumulators
+// (N = 128) let the row-dot epilogue of tile j overlap the MMAs of tile j+1.
+//   TMEM: [0,128) A_hi, [128,256) A_lo, [256,384) / [384,512) accumulators.
+constexpr int FTS_STAGES = 3;
+constexpr int FTS_KPS = 2;             // K blocks per pipeline stage
+constexpr int FTS_B_TILE = 128 * 128;  // 16 KiB per hi / lo per K block
+constexpr int FTS_THREADS = 192;       // TMA, MMA, 4 epilogue (+A loader) warps
+
+struct FwdTsParams {
+    TcArgs a;
+    int mt_per_frame, nt_per_group;
+    int amax;
+    const uint32_t *fa_hi, *fa_lo;  // [T*Mk][Kf/2] packed fp16 pairs
+    const float2 *p0p;
+    float2 *kdp;  // [G][T][Mk][Cp]
+    const float *scales;
+    const int *gate;
+    int exp_flags;  // profiling: 1 no MMA, 2 no TMA, 4 no epilogue math
+    unsigned long long *trace;  // optional [grid][32] globaltimer stamps
+};
+
+template <int CP>
+__global__ void __launch_bounds__(FTS_THREADS, 1)
+    k_tc_forward_ts(const __grid_constant__ CUtensorMap tmB_hi,
+                    const __grid_constant__ CUtensorMap tmB_lo, FwdTsParams P) {
+    using namespace sm100;
+    if (P.gate && !*P.gate) return;
+    constexpr int XS = 64 / CP;  // x values per 128-row B tile
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    // A stage carries kps K blocks ([hi | lo] per block): each barrier wait of
+    // the MMA thread (~200+ cycles even when already satisfied) then covers
+    // kps x 768 MMA cycles
+    constexpr int STAGE = FTS_KPS * 2 * FTS_B_TILE;
+    const int kps = (P.a.Kf / 64) % FTS_KPS == 0 ? FTS_KPS : 1;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + FTS_STAGES * STAGE);
+    uint64_t *empty = full + FTS_STAGES;
+    uint64_t *tfull = empty + FTS_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *a_ready = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mtile = blockIdx.x;
+    const int t = mtile / P.mt_per_frame;
+    const int nt0 = blockIdx.y * P.nt_per_group, nt1 = nt0 + P.nt_per_group;
+    const int nkb = P.a.Kf / 64;
+    unsigned long long *tr =
+        P.trace ? P.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmB_hi);
+        tma_prefetch(&tmB_lo);
+        for (int s = 0; s < FTS_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init(a_ready, 4);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int nt = nt0; nt < nt1; ++nt) {
+                const int brow = t * P.a.Nf + nt * 128;
+                for (int kb = 0; kb < nkb; kb += kps, ++it) {
+                    const int s = it % FTS_STAGES;
+                    const uint32_t ph = (it / FTS_STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *st = smem + s * STAGE;
+                    mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : kps * 2 * FTS_B_TILE);
+                    if (!(P.exp_flags & 2)) {
+                        for (int u = 0; u < kps; ++u) {
+                            uint8_t *sb = st + u * 2 * FTS_B_TILE;
+                            tma_load_2d(sb, &tmB_hi, &full[s], (kb + u) * 64, brow);
+                            tma_load_2d(sb + FTS_B_TILE, &tmB_lo, &full[s], (kb + u) * 64, brow);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(128, 128);
+            mbar_wait(a_ready, 0);
+            tc_fence_after();
+            if (tr) tr[2] = gtimer();
+            const uint32_t a_hi = tmem, a_lo = tmem + 128;
+            int it = 0, tc = 0;
+            for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+                const int ab = tc & 1;
+                const uint32_t aph = (tc >> 1) & 1;
+                mbar_wait(&tempty[ab], aph ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + 256 + ab * 128;
+                for (int kb = 0; kb < nkb; kb += kps, ++it) {
+                    const int s = it % FTS_STAGES;
+                    const uint32_t ph = (it / FTS_STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    if (tr && it < 8) tr[8 + it] = gtimer();
+                    for (int u = 0; u < kps; ++u) {
+                        const uint32_t st = smem_u32(smem + s * STAGE + u * 2 * FTS_B_TILE);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint32_t ac = (kb + u) * 32 + kk * 8;
+                            const uint64_t dbh = desc_sw128(st + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
+                            if (P.exp_flags & 1) continue;
+                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, ((kb + u) | kk) != 0);
+                            mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
+                            mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[ab]);
+                if (tr && tc < 4) tr[16 + tc] = gtimer();
+            }
+            if (tr) tr[3] = gtimer();
+        }
+    } else {
+        // warps 2..5: TMEM lane quarter q; lane m = sample row of the tile
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        // ---- A: this sample's P1 row (hi, lo) -> TMEM, once
+        {
+            const int64_t grow = (int64_t)mtile * 128 + row;  // = t*Mk + local row
+            const int ncol = P.a.Kf / 2;
+            const uint4 *gh = reinterpret_cast<const uint4 *>(P.fa_hi + grow * ncol);
+            const uint4 *gl = reinterpret_cast<const uint4 *>(P.fa_lo + grow * ncol);
+            for (int c0 = 0; c0 < ncol; c0 += 32) {
+                uint32_t vh[32], vl[32];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint4 h = __ldg(gh + c0 / 4 + u), l = __ldg(gl + c0 / 4 + u);
+                    vh[4 * u] = h.x; vh[4 * u + 1] = h.y; vh[4 * u + 2] = h.z; vh[4 * u + 3] = h.w;
+                    vl[4 * u] = l.x; vl[4 * u + 1] = l.y; vl[4 * u + 2] = l.z; vl[4 * u + 3] = l.w;
+                }
+                tmem_st32(lane_base + c0, vh);
+                tmem_st32(lane_base + 128 + c0, vl);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_ready);
+            if (tr && threadIdx.x == 64) tr[5] = gtimer();
+        }
+        // ---- per tile: kd[k, c] += sum_x P0[k, x] G[k, (x, c)]
+        const int64_t kloc = (int64_t)(mtile % P.mt_per_frame) * 128 + row;
+        const bool valid = kloc < P.a.M;
+        const float2 *p0row = P.p0p + ((int64_t)t * P.a.Mk + kloc) * P.a.nxp;
+        constexpr int U = CP > 16 ? CP / 16 : 1;
+        float2 acc[CP];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) acc[c] = make_float2(0.f, 0.f);
+        int tc = 0;
+        for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+            const int ab = tc & 1;
+            const uint32_t aph = (tc >> 1) & 1;
+            const int xbase = nt * XS;
+            // this tile's P0 values are loaded before waiting on the MMA
+            float2 p0v[XS];
+#pragma unroll
+            for (int i = 0; i < XS; ++i)
+                p0v[i] = valid ? p0row[xbase + i] : make_float2(0.f, 0.f);
+            mbar_wait(&tfull[ab], aph);
+            tc_fence_after();
+            const uint32_t taddr = lane_base + 256 + ab * 128;
+#pragma unroll
+            for (int chb = 0; chb < 4; chb += U) {
+                if (P.exp_flags & 4) break;
+#pragma unroll
+                for (int h = 0; h < U; ++h) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + (chb + h) * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int j = (chb + h) * 16 + jj;  // complex column in tile
+                        const float2 gv = make_float2(__uint_as_float(r[2 * jj]),
+                                                      __uint_as_float(r[2 * jj + 1]));
+                        cfma(acc[j % CP], p0v[j / CP], gv);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[ab]);
+            if (tr && threadIdx.x == 64 && tc < 4) tr[24 + tc] = gtimer();
+        }
+        if (tr && threadIdx.x == 64) tr[4] = gtimer();
+        if (P.amax) {  // max|kd| for the adjoint's operand scale (order-free)
+            float mx = 0.f;
+            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
+#pragma unroll
+            for (int c = 0; c < CP; ++c)
+                mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(const_cast<float *>(P.scales) + 5),
+                                     __float_as_uint(mx));
+        }
+        if (valid) {
+            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
             float2 *out = P.kdp + (((int64_t)blockIdx.y * P.a.T + t) * P.a.Mk + kloc) * CP;
 #pragma unroll
             for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
@@ -441,7 +641,8 @@ __global__ void k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, flo
         }
         if (kdi) kdi[i] = s;
     }
-    grid_max_scale(v, partials, ticket, 1.f, scales + 2);
+    float m;
+    if (grid_max(v, partials, ticket, m)) scales[5] = m;
 }
 
 // user (T*M, C) k-space -> internal padded layout + sigma_d
@@ -462,7 +663,8 @@ __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *
         }
         kdi[i] = s;
     }
-    grid_max_scale(v, partials, ticket, 1.f, scales + 2);
+    float m;
+    if (grid_max(v, partials, ticket, m)) scales[5] = m;
 }
 
 struct AdjParams {
@@ -470,6 +672,7 @@ struct AdjParams {
     int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs, chain;
     int exp_flags;  // profiling experiments: 1 = no generator math, 2 = no MMA
     int cs;         // cluster size along the (x, c) tiles sharing one B tile
+    unsigned long long *trace;
     const float2 *sens;
     float2 *ws;  // [S][T][nx][ny]
     const float *scales;
@@ -523,6 +726,13 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     const int nkb = kb1 - kb0;
     const int chain = P.chain;
     const int nchain = (nkb + chain - 1) / chain;
+    unsigned long long *tr = P.trace ? P.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) *
+                                                   gridDim.x + blockIdx.x) * 32
+                                     : nullptr;
+    if (tr && threadIdx.x == 0) {
+        tr[0] = gtimer();
+        tr[30] = clock64();
+    }
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmB_hi);
@@ -613,6 +823,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 }
                 mma_commit(acc_full);
             }
+            if (tr) {
+                tr[1] = gtimer();
+                tr[31] = clock64();
+            }
         }
     } else if (warp >= 4 && warp < 8) {
         // ---- generator warpgroup: lane quarter q, row m = (x, c, part)
@@ -621,7 +835,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-        const float sg = P.scales[2];
+        const float sg = pow2_scale(P.scales[5]);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % ADJ_STAGES;
             const uint32_t ph = (i / ADJ_STAGES) & 1;
@@ -663,7 +877,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-        const float inv = P.scales[3];
+        const float inv = 1.f / pow2_scale(P.scales[5]);
         for (int ch = 0; ch < nchain; ++ch) {
             mbar_wait(acc_full, ch & 1);
             tc_fence_after();
@@ -826,6 +1040,25 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     while (G < tc.nt && mtiles * G < 2 * 148 && tc.nt % (2 * G) == 0) G *= 2;
     tc.G = G;
     tc.nt_per_group = tc.nt / G;
+    // A-stationary forward: 128-row B tiles; groups of tiles per CTA chosen
+    // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup)
+    tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS");
+    if (tc.fwd_ts) {
+        const int nt128 = tc.Nf / 128, nkb = tc.Kf / 64;
+        int64_t best = INT64_MAX;
+        for (int g = 1; g <= nt128; ++g) {
+            if (nt128 % g) continue;
+            const int64_t waves = (mtiles * g + 147) / 148;
+            const int64_t cost = waves * ((int64_t)(nt128 / g) * nkb * 768 + 6000);
+            if (cost < best) {
+                best = cost;
+                tc.G_ts = g;
+            }
+        }
+        tc.ntpg_ts = nt128 / tc.G_ts;
+        tc.fts_smem = FTS_STAGES * FTS_KPS * 2 * FTS_B_TILE + 1024 + 256;
+        G = std::max(G, tc.G_ts);
+    }
     // adjoint split-K
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
@@ -856,7 +1089,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.split = S;
     tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
     // clusters of CTAs that share one B tile (same frame, split, y tile)
-    tc.adj_cs = tc.mt_a % 4 == 0 ? 4 : (tc.mt_a % 2 == 0 ? 2 : 1);
+    tc.adj_cs = 1;  // multicast measured no faster (L2 dedups the shared B tile)
     if (const char *e = getenv("CSR_ADJ_CLUSTER")) {
         int v = atoi(e);
         if ((v == 1 || v == 2 || v == 4) && tc.mt_a % v == 0) tc.adj_cs = v;
@@ -883,6 +1116,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     TCA(tc.xb_lo, xb * 2, ws_bytes);
     TCA(tc.kdp, (size_t)G * T * tc.Mk * Cp * 8, ws_bytes);
     TCA(tc.kdi, (size_t)T * tc.Mk * Cp * 8, ws_bytes);
+    cudaMemsetAsync(tc.kdi, 0, (size_t)T * tc.Mk * Cp * 8, st);
     TCA(tc.ws, (size_t)S * T * nx * ny * 8, ws_bytes);
     TCA(tc.scales, 64, ws_bytes);
     TCA(tc.red, 4 * 148 * 8, ws_bytes);
@@ -905,6 +1139,8 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_fa_lo, tc.fa_lo, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
               tmap_f16_2d(&tc.tm_xb_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
+              tmap_f16_2d(&tc.tm_xb128_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
+              tmap_f16_2d(&tc.tm_xb128_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
               tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
               tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
@@ -916,42 +1152,89 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
         default: break;
     }
+    if (getenv("CSR_TRACE")) {
+        if (tc_alloc(allocs, &p, 4096 * 32 * 8, ws_bytes, st)) return 2;
+        tc.trace = (unsigned long long *)p;
+        cudaMemsetAsync(tc.trace, 0, 4096 * 32 * 8, st);
+    }
+    set_smem(k_tc_forward_ts<4>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<8>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<16>, tc.fts_smem);
     tc.enabled = true;
     return 0;
 }
 
 // image (T,nx,ny) -> kd.  user != nullptr: also write the (T*M, C) layout
-inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user,
-                      cudaStream_t st, const int *gate) {
+// image -> k-space.  user != nullptr: also write the (T*M, C) layout.
+// in_loop: inside the native CG loop the producer of img (k_admm_rhs /
+// k_cg_d) already left max|img| in scales[6], and with a single tile group
+// the forward writes the k-space buffer directly (atomic max into scales[5])
+// instead of going through partials + k_tc_sum_kd.
+inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t st,
+                      const int *gate, bool in_loop = false) {
     TcArgs a = tc_args(tc);
     const int64_t n = (int64_t)tc.T * tc.nx * tc.ny;
-    k_tc_absmax_img<<<reduce_blocks(n, 256), 256, 0, st>>>(img, n, tc.red, tc.tick, tc.scales,
-                                                           gate);
+    if (!in_loop)
+        k_tc_absmax_img<<<reduce_blocks(n, 256), 256, 0, st>>>(img, n, tc.red, tc.tick,
+                                                               tc.scales, gate);
     {
         int64_t total = (int64_t)tc.T * tc.nxp * tc.Cp * tc.nyp;
         int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
         k_tc_prep_x<<<nb, 256, 0, st>>>(a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate);
     }
-    FwdParams P;
-    P.a = a;
-    P.mt_per_frame = tc.mt_f;
-    P.nt_per_group = tc.nt_per_group;
-    P.p0p = tc.p0p;
-    P.kdp = tc.kdp;
-    P.scales = tc.scales;
-    P.gate = gate;
-    dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)tc.G);
-    switch (tc.Cp) {
-        case 4: k_tc_forward<4><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-        case 8: k_tc_forward<8><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-        default: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+    const int G = tc.fwd_ts ? tc.G_ts : tc.G;
+    const bool direct = in_loop && !user && G == 1;
+    float2 *kdp = direct ? tc.kdi : tc.kdp;
+    if (tc.fwd_ts) {
+        FwdTsParams P;
+        P.a = a;
+        P.mt_per_frame = tc.mt_f;
+        P.nt_per_group = tc.ntpg_ts;
+        P.amax = direct ? 1 : 0;
+        P.fa_hi = reinterpret_cast<const uint32_t *>(tc.fa_hi);
+        P.fa_lo = reinterpret_cast<const uint32_t *>(tc.fa_lo);
+        P.p0p = tc.p0p;
+        P.kdp = kdp;
+        P.scales = tc.scales;
+        P.gate = gate;
+        P.exp_flags = getenv("CSR_FEXP") ? atoi(getenv("CSR_FEXP")) : 0;
+        P.trace = tc.trace;
+        dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
+        switch (tc.Cp) {
+            case 4: k_tc_forward_ts<4><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            case 8: k_tc_forward_ts<8><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            default: k_tc_forward_ts<16><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+        }
+    } else {
+        FwdParams P;
+        P.a = a;
+        P.mt_per_frame = tc.mt_f;
+        P.nt_per_group = tc.nt_per_group;
+        P.amax = direct ? 1 : 0;
+        P.p0p = tc.p0p;
+        P.kdp = kdp;
+        P.scales = tc.scales;
+        P.gate = gate;
+        dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
+        switch (tc.Cp) {
+            case 4: k_tc_forward<4><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            case 8: k_tc_forward<8><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            default: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+        }
     }
-    {
+    if (!direct) {
         int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-        k_tc_sum_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, tc.G, tc.kdp, tc.kdi, user,
+        k_tc_sum_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, G, tc.kdp, tc.kdi, user,
                                                                tc.red, tc.tick, tc.scales, gate);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// launches tc_forward makes (for the kernel-count bookkeeping)
+inline int tc_forward_launches(const TcPlan &tc, bool in_loop, bool user) {
+    const int G = tc.fwd_ts ? tc.G_ts : tc.G;
+    const bool direct = in_loop && !user && G == 1;
+    return (in_loop ? 0 : 1) + 2 + (direct ? 0 : 1);
 }
 
 // kd already in tc.kdi (with sigma_d) when user == nullptr; else load it
@@ -970,6 +1253,7 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.chain = TC_MAX_CHAIN;
     P.exp_flags = getenv("CSR_EXP") ? atoi(getenv("CSR_EXP")) : 0;
     P.cs = tc.adj_cs;
+    P.trace = tc.trace;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
     P.stage_bytes = tc.adj_stage;
