@@ -35,6 +35,9 @@ from harness.configs import CONFIGS, make_problem, nudft_flops_per_cg  # noqa: E
 PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 METRIC = "ADMM iters/s"
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+# kernel, from one `ncu --set full` capture (profiles/r01_ncu_adjoint_c*.txt)
+TRAFFIC = {}
 
 
 def peaks():
@@ -273,19 +276,30 @@ def run_ours(args, cfg, world, rank, local):
     value = args.steps / t_solve
     kpi = stats.kernels_per_iter
 
-    # roofline: dominant kernel = the NUDFT GEMMs (forward / adjoint)
-    kt = time_kernels(op, prob)
+    # roofline: dominant kernel = the NUDFT GEMMs (forward / adjoint), timed
+    # live inside the timed ADMM iterations (events around every launch,
+    # recorded in the iteration graph on the plan stream)
+    fm, am = ctypes.c_double(), ctypes.c_double()
+    fn, an = ctypes.c_int64(), ctypes.c_int64()
+    _native.call("csr_plan_kernel_times", op.plan, ctypes.byref(fm), ctypes.byref(am),
+                 ctypes.byref(fn), ctypes.byref(an))
+    kt = {"forward": fm.value, "adjoint": am.value}
+    kn = {"forward": fn.value, "adjoint": an.value}
+    kt_cold = time_kernels(op, prob)
     flops_launch = 8.0 * op.n_coils * op.m_per_frame * op.nx * op.ny * op.n_frames
     pk, src = peaks()
     dom = max(kt, key=kt.get)
-    achieved = flops_launch / (kt[dom] * 1e-3) / 1e12
+    achieved = flops_launch / (kt[dom] * 1e-3) / 1e12 if kt[dom] > 0 else 0.0
+    step_ms = 1e3 * t_solve / args.steps
     roofline = {"bound": "tensor", "kernel": f"nudft_{dom}",
                 "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": None,
+                "frac": achieved / pk["bf16_tflops"], "traffic": TRAFFIC.get(cfg),
                 "peak_source": f"{src} dense bf16",
                 "flops_per_launch": flops_launch,
-                "ms_per_launch": kt,
-                "share_of_step": {k: 5 * v / (1e3 * t_solve / args.steps) for k, v in kt.items()}}
+                "tensor_flops_per_launch": 3 * flops_launch,
+                "ms_per_launch": kt, "launches_timed": kn,
+                "ms_per_launch_cold": kt_cold,
+                "share_of_step": {k: kn[k] / args.steps * v / step_ms for k, v in kt.items()}}
 
     # e2e through the public API with pinned host buffers
     e2e = None

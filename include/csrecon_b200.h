@@ -168,6 +168,14 @@ int csr_admm_run(csr_plan *plan, const csr_admm_params *params,
 int csr_plan_set_timing(csr_plan *plan, void *flush_buf, int64_t flush_bytes,
                         float *iter_ms);
 
+/* Benchmark: average device time per launch of the tensor-core NUDFT
+ * forward and adjoint GEMM kernels inside the ADMM loop of the last timed
+ * csr_admm_run (first-CTA start to last-CTA end, %globaltimer stamps taken
+ * by the kernels themselves, so the timed graph is unchanged), and how many
+ * launches were averaged.  Zero counts on the SIMT path. */
+int csr_plan_kernel_times(csr_plan *plan, double *fwd_ms, double *adj_ms,
+                          int64_t *n_fwd, int64_t *n_adj);
+
 /* adjoint_reconstruct (solver.py:363-406): image = allreduce(F^H d). */
 int csr_adjoint_reconstruct(csr_plan *plan, const void *kdata, void *image,
                             void *stream);

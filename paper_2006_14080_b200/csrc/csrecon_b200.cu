@@ -689,6 +689,8 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         p->graph_key = key;
     }
     const bool timed = p->iter_ms != nullptr;
+    if (timed && p->tc.probe)
+        CU(cudaMemsetAsync(p->tc.probe, 0, 8 * sizeof(unsigned long long), st));
     if (timed) {
         while ((int)p->iter_ev.size() < 2 * prm->admm_max_iters) {
             cudaEvent_t e;
@@ -766,6 +768,21 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
 int csr_debug_trace(csr_plan *p, unsigned long long *host, int64_t n) {
     if (!p || !p->tc.trace) return fail(CSR_ERR_ARG, "no trace buffer (set CSR_TRACE)");
     CU(cudaMemcpy(host, p->tc.trace, std::min<int64_t>(n, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
+    return CSR_OK;
+}
+
+int csr_plan_kernel_times(csr_plan *p, double *fwd_ms, double *adj_ms, int64_t *n_fwd,
+                          int64_t *n_adj) {
+    if (!p || !fwd_ms || !adj_ms || !n_fwd || !n_adj) return fail(CSR_ERR_ARG, "null argument");
+    unsigned long long h[8] = {};
+    if (p->tc.probe) {
+        CU(cudaStreamSynchronize(p->stream));
+        CU(cudaMemcpy(h, p->tc.probe, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    *n_fwd = (int64_t)h[3];
+    *n_adj = (int64_t)h[7];
+    *fwd_ms = h[3] ? 1e-6 * (double)h[2] / (double)h[3] : 0.0;
+    *adj_ms = h[7] ? 1e-6 * (double)h[6] / (double)h[7] : 0.0;
     return CSR_OK;
 }
 
