@@ -14,6 +14,11 @@ from .errors import (CgDivergenceError, MemoryBudgetError, NativeError,
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcsrecon_b200.so")
+# profiling variants (tools/build_variants.py) live next to the product
+# library; CSR_VARIANT=<name> loads paper_2006_14080_b200/variants/<name>.so
+if os.environ.get("CSR_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "variants",
+                            os.environ["CSR_VARIANT"] + ".so")
 
 CSR_OK, CSR_ERR_SHAPE, CSR_ERR_OOM, CSR_ERR_CUDA, CSR_ERR_NCCL, \
     CSR_ERR_NONFINITE, CSR_ERR_ARG = range(7)

@@ -46,27 +46,32 @@ def up_to_date():
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile the library; `defines`/`out` build a profiling variant
+    (tools/build_variants.py) instead of the product library."""
+    if out is None and not defines and not force and up_to_date():
         return OUT
+    out = out or OUT
     nccl = nccl_root()
-    cmd = (["nvcc"] + ARCH + ["-O3", "-lineinfo", "-std=c++17", "-shared",
+    cmd = (["nvcc"] + ARCH + [f"-D{d}" for d in defines] +
+           ["-O3", "-lineinfo", "-std=c++17", "-shared",
                               "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                               "-I", os.path.join(nccl, "include"),
                               "-I", os.path.join(REPO, "include"),
                               os.path.join(CSRC, "csrecon_b200.cu"),
                               "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
                               "-Xlinker", "-rpath," + os.path.join(nccl, "lib"),
-                              "-o", OUT + ".tmp"])
+                              "-o", out + ".tmp"])
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode:
         sys.stderr.write(res.stdout + res.stderr)
     if res.returncode:
         raise RuntimeError(f"nvcc failed ({res.returncode})")
-    os.replace(OUT + ".tmp", OUT)
-    with open(os.path.join(HERE, "ptxas.log"), "w") as f:
+    os.replace(out + ".tmp", out)
+    with open(out[:-3] + ".ptxas.log" if out != OUT else os.path.join(HERE, "ptxas.log"),
+              "w") as f:
         f.write(res.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -57,7 +57,7 @@ struct TcPlan {
     unsigned long long *probe = nullptr;   // [2][4] live timing slots: forward, adjoint
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags
     int G_ts = 1, ntpg_ts = 1, fts_smem = 0;
-    int raw_bytes = 0, adj_stage = 0, fwd_smem = 0, adj_smem = 0, adj_cs = 1;
+    int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0, adj_cs = 1;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
@@ -241,8 +241,11 @@ __device__ __forceinline__ void probe_exit(unsigned long long *pr) {
     }
 }
 
+// (offset arithmetic on the __shared__ pointer itself keeps the compiler's
+// address-space inference: LDS, not generic LD, for the smem operands)
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
-    return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
 template <int CP>
@@ -695,10 +698,29 @@ __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *
     if (grid_max(v, partials, ticket, m)) scales[5] = m;
 }
 
+__device__ __forceinline__ void tmem_st_n(uint32_t a, const uint32_t (&r)[32]) {
+    sm100::tmem_st32(a, r);
+}
+__device__ __forceinline__ void tmem_st_n(uint32_t a, const uint32_t (&r)[16]) {
+    sm100::tmem_st16(a, r);
+}
+
+// CTA-0 per-K-block timeline for tools/trace_adj_tl.py (-DADJ_TIMELINE=1)
+#if ADJ_TIMELINE
+#define ADJ_TL(slot, cond)                                                      \
+    if (tr && (cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && \
+        i < 256)                                                                \
+    tr[65536 + 4 * i + (slot)] = gtimer()
+#else
+#define ADJ_TL(slot, cond) \
+    do {                   \
+    } while (0)
+#endif
+
 struct AdjParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
     TcArgs a;
-    int S, kb_per_split, kb_total, raw_bytes, stage_bytes, xs, chain;
+    int S, kb_per_split, kb_total, raw_bytes, raw_stage, n_raw, chain;
     int exp_flags;  // profiling experiments: 1 = no generator math, 2 = no MMA
     int cs;         // cluster size along the (x, c) tiles sharing one B tile
     unsigned long long *trace;
@@ -708,9 +730,45 @@ struct AdjParams {
     const int *gate;
 };
 
-constexpr int ADJ_STAGES = 4;
-constexpr int ADJ_B_TILE = 128 * 128;   // 16 KiB
-constexpr int ADJ_THREADS = 384;        // WG0: TMA, MMA; WG1: generator; WG2: epilogue
+constexpr int ADJ_STAGES = 4;             // B tiles in smem = A stages in TMEM
+constexpr int ADJ_B_TILE = 128 * 128;     // 16 KiB (one of hi / lo)
+constexpr int ADJ_B_STAGE = 2 * ADJ_B_TILE;
+constexpr int ADJ_MAX_RAW = 8;            // generator-input ring depth (max)
+// warps: 0 B-ring TMA, 1 MMA, 2 raw-ring TMA, 3 idle, 4 .. 4+GW-1 generators
+// (GW / 4 per TMEM lane quarter, each writing SPW samples of a K block),
+// then four epilogue warps
+#ifndef ADJ_GW
+#define ADJ_GW 4
+#endif
+// Barrier waits: the long ones (producers, epilogue) sleep on the barrier
+// (ADJ_SLEEP_SLOW), the latency-critical ones (MMA issuer, generators) spin
+// unless ADJ_SLEEP_FAST.
+#ifndef ADJ_MERGED_N256
+#define ADJ_MERGED_N256 1
+#endif
+#ifndef ADJ_SLEEP_SLOW
+#define ADJ_SLEEP_SLOW 1
+#endif
+#ifndef ADJ_SLEEP_FAST
+#define ADJ_SLEEP_FAST 0
+#endif
+__device__ __forceinline__ void wait_slow(uint64_t *b, uint32_t ph) {
+#if ADJ_SLEEP_SLOW
+    sm100::mbar_wait_sleep(b, ph);
+#else
+    sm100::mbar_wait(b, ph);
+#endif
+}
+__device__ __forceinline__ void wait_fast(uint64_t *b, uint32_t ph) {
+#if ADJ_SLEEP_FAST
+    sm100::mbar_wait_sleep(b, ph);
+#else
+    sm100::mbar_wait(b, ph);
+#endif
+}
+constexpr int ADJ_SPW = 32 * 4 / ADJ_GW;
+constexpr int ADJ_W_EPI = 4 + ADJ_GW;
+constexpr int ADJ_THREADS = (ADJ_W_EPI + 4) * 32;
 constexpr int ADJ_SUM_LD = 129;                       // padded row (floats)
 constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 running sums [y][lane]
 
@@ -719,12 +777,23 @@ constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 running sums [y][l
 // (x, c) columns) x 128 pixel rows y; K = 32 samples (64 fp16) per block.
 // The generator warpgroup writes W' straight into tensor memory with
 // tcgen05.st, so shared memory only carries the static factor conj(P1)^T
-// (TMA, 128B swizzle) and the P0 / d inputs of the generator (4 stages).
+// (TMA, 128B swizzle) and the P0 / d inputs of the generator.
+//
+// Three rings keep the tensor core fed:
+//   B ring   (4 smem stages): TMA (warp 0) -> MMA; freed by the MMA commit.
+//   raw ring (n_raw smem stages, deeper): TMA (warp 2) -> generators; freed
+//            as soon as the generators have the values in registers, so the
+//            inputs of block i are resident long before its A stage frees.
+//   A ring   (4 TMEM stages): generators -> MMA; freed by the same MMA
+//            commit as the B stage of that block.
+// A generator therefore waits only for the MMA that last used its TMEM
+// stage, not for a TMA round trip behind it.
+//
 // The k range is cut into accumulation chains of <= chain blocks (the
 // tensor core truncates on every fp32 accumulate); the epilogue warpgroup
 // drains each chain into an fp32 running sum in shared memory and frees the
-// accumulator, and after the last chain combines coils and writes one
-// split-K partial image.
+// accumulator.  After the last chain all warps combine coils and
+// write one split-K partial image.
 //   TMEM columns: [0,128) hi*hi accumulator, [128,256) hi*lo + lo*hi
 //   corrections, [256,512) four A stages of (hi 32 | lo 32).
 template <int CP>
@@ -739,12 +808,15 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     constexpr int XS = 64 / CP;  // x values per tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    float *sum_s = reinterpret_cast<float *>(smem + ADJ_STAGES * P.stage_bytes);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ADJ_STAGES * P.stage_bytes +
+    uint8_t *raw_base = smem + ADJ_STAGES * ADJ_B_STAGE;
+    float *sum_s = reinterpret_cast<float *>(raw_base + P.n_raw * P.raw_stage);
+    uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sum_s) +
                                                   ADJ_SUM_BYTES);
     uint64_t *gen = full + ADJ_STAGES;
     uint64_t *empty = gen + ADJ_STAGES;
-    uint64_t *acc_full = empty + ADJ_STAGES;
+    uint64_t *rfull = empty + ADJ_STAGES;
+    uint64_t *rempty = rfull + ADJ_MAX_RAW;
+    uint64_t *acc_full = rempty + ADJ_MAX_RAW;
     uint64_t *acc_empty = acc_full + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
 
@@ -756,6 +828,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     const int nkb = kb1 - kb0;
     const int chain = P.chain;
     const int nchain = (nkb + chain - 1) / chain;
+    const int NR = P.n_raw;
     unsigned long long *tr = P.trace ? P.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) *
                                                    gridDim.x + blockIdx.x) * 32
                                      : nullptr;
@@ -771,8 +844,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         tma_prefetch(&tmKd);
         for (int s = 0; s < ADJ_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&gen[s], 4);
+            mbar_init(&gen[s], ADJ_GW);
             mbar_init(&empty[s], P.cs);  // every cluster CTA's MMA frees stage s
+        }
+        for (int r = 0; r < NR; ++r) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&rempty[r], ADJ_GW);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
@@ -784,23 +861,20 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     if (P.cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tx_bytes = ((P.exp_flags & 8) ? 0 : 2 * ADJ_B_TILE) +
-                              ((P.exp_flags & 16) ? 0 : P.raw_bytes);
     const uint32_t crank = P.cs > 1 ? cluster_ctarank() : 0;
-
     const uint16_t cmask = (uint16_t)((1u << P.cs) - 1);
 
     if (warp == 0) {
+        // ---- B ring producer: conj(P1)^T hi / lo tiles
         if (lane == 0) {
             const int brow = t * P.a.nyA + nt * 128;
+            const uint32_t tx = (P.exp_flags & 8) ? 0 : ADJ_B_STAGE;
             for (int i = 0; i < nkb; ++i) {
                 const int kb = kb0 + i;
                 const int s = i % ADJ_STAGES;
-                const uint32_t ph = (i / ADJ_STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t *st = smem + s * P.stage_bytes;
-                uint8_t *raw = st + 2 * ADJ_B_TILE;
-                mbar_arrive_expect_tx(&full[s], tx_bytes);
+                wait_slow(&empty[s], ((i / ADJ_STAGES) & 1) ^ 1);
+                uint8_t *st = smem + s * ADJ_B_STAGE;
+                mbar_arrive_expect_tx(&full[s], tx);
                 if (P.exp_flags & 8) {
                 } else if (P.cs > 1) {
                     // this CTA fetches rows [crank*R, (crank+1)*R) of the shared
@@ -814,28 +888,46 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                     tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
                     tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
                 }
+            }
+        }
+    } else if (warp == 2) {
+        // ---- raw ring producer: P0 rows of the tile's x values, and d
+        if (lane == 0) {
+            const uint32_t tx = (P.exp_flags & 16) ? 0 : P.raw_bytes;
+            for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
+                const int kb = kb0 + i;
+                wait_slow(&rempty[r], rph ^ 1);
+                uint8_t *raw = raw_base + r * P.raw_stage;
+                mbar_arrive_expect_tx(&rfull[r], tx);
                 if (!(P.exp_flags & 16)) {
-                    tma_load_3d(raw, &tmP0, &full[s], mt * XS, kb * 32, t);
-                    tma_load_3d(raw + 32 * XS * 8, &tmKd, &full[s], 0, kb * 32, t);
+                    tma_load_3d(raw, &tmP0, &rfull[r], mt * XS, kb * 32, t);
+                    tma_load_3d(raw + 32 * XS * 8, &tmKd, &rfull[r], 0, kb * 32, t);
+                }
+                if (++r == NR) {
+                    r = 0;
+                    rph ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
+        // ---- MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, 128);
+            constexpr uint32_t idesc256 = idesc_f16(128, 256);
             const uint32_t d_hi = tmem, d_lo = tmem + 128;
             int i = 0;
             for (int ch = 0; ch < nchain; ++ch) {
-                mbar_wait(acc_empty, (ch & 1) ^ 1);
+                wait_fast(acc_empty, (ch & 1) ^ 1);
                 tc_fence_after();
                 const int iend = min(nkb, i + chain);
                 for (int i0 = i; i < iend; ++i) {
                     const int s = i % ADJ_STAGES;
                     const uint32_t ph = (i / ADJ_STAGES) & 1;
-                    mbar_wait(&full[s], ph);
-                    mbar_wait(&gen[s], ph);
+                    wait_fast(&gen[s], ph);
+                    ADJ_TL(0, true);
+                    wait_fast(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * P.stage_bytes);
+                    const uint32_t st = smem_u32(smem + s * ADJ_B_STAGE);
                     const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
@@ -843,10 +935,19 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                         const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
                         const uint32_t acc = (i != i0) || (kk != 0);
                         if (P.exp_flags & 2) continue;
+#if ADJ_MERGED_N256
+                        // B' = [hi_B ; lo_B] is one 256-row SW128 tile: a single
+                        // N = 256 MMA writes hi*hi_B to D_hi and hi*lo_B to D_lo
+                        (void)dbl;
+                        mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc256, acc);
+                        mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
+#else
                         mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, acc);
                         mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, acc);
                         mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
+#endif
                     }
+                    // frees B stage s (TMA) and A stage s (generators)
                     if (P.exp_flags & 32) mbar_arrive(&empty[s]);
                     else if (P.cs > 1) mma_commit_mc(&empty[s], cmask);
                     else mma_commit(&empty[s]);
@@ -858,58 +959,84 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 tr[31] = clock64();
             }
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ---- generator warpgroup: lane quarter q, row m = (x, c, part)
+    } else if (warp >= 4 && warp < ADJ_W_EPI) {
+        // ---- generators: lane quarter q, row m = (x, c, part), samples
+        // [h*SPW, (h+1)*SPW) of every K block
         const int q = warp & 3;
+        const int h = (warp - 4) >> 2;
         const int m = q * 32 + lane;
         const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const float sg = pow2_scale(P.scales[5]);
-        for (int i = 0; i < nkb; ++i) {
+        for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
             const int s = i % ADJ_STAGES;
-            const uint32_t ph = (i / ADJ_STAGES) & 1;
-            mbar_wait(&full[s], ph);
-            const float2 *p0s = reinterpret_cast<const float2 *>(smem + s * P.stage_bytes +
-                                                                 2 * ADJ_B_TILE);
+            wait_fast(&rfull[r], rph);
+            ADJ_TL(1, lane == 0 && warp == 4);
+            const float2 *p0s = reinterpret_cast<const float2 *>(raw_base + r * P.raw_stage);
             const float2 *ds = p0s + 32 * XS;
-            uint32_t hv[32], lv[32];
+            uint32_t hv[ADJ_SPW], lv[ADJ_SPW];
             if (P.exp_flags & 1) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) hv[k] = lv[k] = 0u;
+                for (int k = 0; k < ADJ_SPW; ++k) hv[k] = lv[k] = 0u;
             } else
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
+            for (int kk = 0; kk < ADJ_SPW; ++kk) {
+                const int k = h * ADJ_SPW + kk;
+#if ADJ_GEN_VARIANT == 2  // profiling: no shared-memory operands
+                const float2 p = make_float2((float)k, (float)xl);
+                const float2 d = make_float2((float)c, (float)(k + i));
+#else
                 const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
+#endif
                 const float wr = sg * (p.x * d.x + p.y * d.y);
                 const float wi = sg * (p.x * d.y - p.y * d.x);
                 // Re row (part 0): (wr, -wi); Im row (part 1): (wi, wr)
                 const float e0 = part ? wi : wr, e1 = part ? wr : -wi;
+#if ADJ_GEN_VARIANT == 1  // profiling: no fp16 conversion
+                hv[kk] = __float_as_uint(e0);
+                lv[kk] = __float_as_uint(e1);
+#elif ADJ_GEN_VARIANT == 3  // profiling: hi conversion only
+                const __half2 hh = __floats2half2_rn(e0, e1);
+                hv[kk] = *reinterpret_cast<const uint32_t *>(&hh);
+                lv[kk] = hv[kk] ^ 0x80008000u;
+#else
                 const __half2 hh = __floats2half2_rn(e0, e1);
                 const float2 hf = __half22float2(hh);
                 const __half2 ll = __floats2half2_rn(e0 - hf.x, e1 - hf.y);
-                hv[k] = *reinterpret_cast<const uint32_t *>(&hh);
-                lv[k] = *reinterpret_cast<const uint32_t *>(&ll);
+                hv[kk] = *reinterpret_cast<const uint32_t *>(&hh);
+                lv[kk] = *reinterpret_cast<const uint32_t *>(&ll);
+#endif
             }
+            // inputs are in registers: hand the raw stage back to the TMA
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[r]);
+            if (++r == NR) {
+                r = 0;
+                rph ^= 1;
+            }
+            // A stage s is free once the MMAs of block i - 4 completed
+            wait_fast(&empty[s], ((i / ADJ_STAGES) & 1) ^ 1);
+            ADJ_TL(2, lane == 0 && warp == 4);
+            tc_fence_after();
             if (!(P.exp_flags & 4)) {
-                tmem_st32(lane_base + 256 + 64 * s, hv);
-                tmem_st32(lane_base + 256 + 64 * s + 32, lv);
+                const uint32_t col = lane_base + 256 + 64 * s + h * ADJ_SPW;
+                tmem_st_n(col, hv);
+                tmem_st_n(col + 32, lv);
                 tmem_st_wait();
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[s]);
+            ADJ_TL(3, lane == 0 && warp == 4);
         }
-    } else if (warp >= 8) {
-        // ---- epilogue warpgroup
+    } else if (warp >= ADJ_W_EPI) {
+        // ---- epilogue warpgroup: drain every chain into the running sums
         const int q = warp & 3;
         const int m = q * 32 + lane;
-        const int j = m >> 1, part = m & 1;
-        const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-        const float inv = 1.f / pow2_scale(P.scales[5]);
         for (int ch = 0; ch < nchain; ++ch) {
-            mbar_wait(acc_full, ch & 1);
+            wait_slow(acc_full, ch & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int cb = 0; cb < 4; ++cb) {
@@ -930,43 +1057,41 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 }
             }
         }
-        // ---- combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y)
-        // thread e handles pixel row y = e for every x of the tile, reading the
-        // transposed sums (padded rows: conflict-free) and the coil maps with
-        // y-coalesced loads
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (P.exp_flags & 64) goto done;
-        {
-            const int e = threadIdx.x - 256;
-            const int y = nt * 128 + e;
-            const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
-            float2 *wbase = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
-            const float *row = sum_s + e * ADJ_SUM_LD;
-            if (y < P.a.ny) {
-#pragma unroll 2
-                for (int xq = 0; xq < XS; ++xq) {
-                    const int xg = mt * XS + xq;
-                    if (xg >= P.a.nx) break;
-                    float ar = 0.f, ai = 0.f;
-#pragma unroll
-                    for (int cc = 0; cc < CP; ++cc) {
-                        if (cc < P.a.C) {
-                            const float re = row[2 * (xq * CP + cc)];
-                            const float im = row[2 * (xq * CP + cc) + 1];
-                            const float2 sv = __ldg(P.sens + (int64_t)cc * nxy +
-                                                    (int64_t)xg * P.a.ny + y);
-                            ar += sv.x * re + sv.y * im;
-                            ai += sv.x * im - sv.y * re;
-                        }
-                    }
-                    wbase[(int64_t)xg * P.a.ny + y] = make_float2(ar * inv, ai * inv);
-                }
-            }
-        }
-    done:;
     }
     __syncthreads();
+    // ---- combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y), all
+    // warps: thread e handles pixel row y = e % 128 for the x values
+    // xq = e / 128 (mod warps / 4) of the tile, reading the transposed sums (padded
+    // rows: conflict-free) and the coil maps with y-coalesced loads
+    if (!(P.exp_flags & 64)) {
+        const float inv = 1.f / pow2_scale(P.scales[5]);
+        const int e = threadIdx.x & 127, grp = threadIdx.x >> 7;
+        const int y = nt * 128 + e;
+        const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
+        float2 *wbase = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
+        const float *row = sum_s + e * ADJ_SUM_LD;
+        if (y < P.a.ny) {
+            for (int xq = grp; xq < XS; xq += ADJ_THREADS / 128) {
+                const int xg = mt * XS + xq;
+                if (xg >= P.a.nx) break;
+                float ar = 0.f, ai = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < CP; ++cc) {
+                    if (cc < P.a.C) {
+                        const float re = row[2 * (xq * CP + cc)];
+                        const float im = row[2 * (xq * CP + cc) + 1];
+                        const float2 sv = __ldg(P.sens + (int64_t)cc * nxy +
+                                                (int64_t)xg * P.a.ny + y);
+                        ar += sv.x * re + sv.y * im;
+                        ai += sv.x * im - sv.y * re;
+                    }
+                }
+                wbase[(int64_t)xg * P.a.ny + y] = make_float2(ar * inv, ai * inv);
+            }
+        }
+    }
     if (P.cs > 1) cluster_sync();  // no CTA leaves while peers may still signal it
+    __syncthreads();
     probe_exit(P.probe);
     if (warp == 1) {
         tc_fence_after();
@@ -1125,9 +1250,15 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         int v = atoi(e);
         if ((v == 1 || v == 2 || v == 4) && tc.mt_a % v == 0) tc.adj_cs = v;
     }
-    tc.adj_stage = (2 * ADJ_B_TILE + tc.raw_bytes + 1023) / 1024 * 1024;
+    tc.adj_stage = (tc.raw_bytes + 127) / 128 * 128;  // raw ring stage
     tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
-    tc.adj_smem = ADJ_STAGES * tc.adj_stage + ADJ_SUM_BYTES + 1024 + 256;
+    {
+        const int fixed = ADJ_STAGES * ADJ_B_STAGE + ADJ_SUM_BYTES + 1024 + 512;
+        tc.adj_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
+        if (const char *e = getenv("CSR_ADJ_NRAW"))
+            tc.adj_nraw = std::max(1, std::min(tc.adj_nraw, atoi(e)));
+        tc.adj_smem = fixed + tc.adj_nraw * tc.adj_stage;
+    }
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
     const size_t fa = (size_t)T * tc.Mk * tc.Kf, ga = (size_t)T * tc.nyA * 2 * tc.Mk;
@@ -1295,8 +1426,8 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.probe = tc.probe ? tc.probe + 4 : nullptr;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
-    P.stage_bytes = tc.adj_stage;
-    P.xs = 64 / tc.Cp;
+    P.raw_stage = tc.adj_stage;
+    P.n_raw = tc.adj_nraw;
     P.sens = tc.sens;
     P.ws = ws;
     P.scales = tc.scales;

@@ -73,6 +73,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #endif
 }
 
+// Wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint elapses) instead of re-issuing try_wait, so a
+// long-waiting role does not take issue slots from the warps that share its
+// SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_wait_hint(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait_hint(bar, parity)) {
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+
 // ---- TMA -------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap *m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
@@ -175,6 +198,19 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// One lane of a converged warp (elect.sync).  Issuing tcgen05.mma from a
+// whole warp under elect_one() keeps the descriptors warp-uniform, so ptxas
+// feeds UTCHMMA from uniform registers instead of wrapping every MMA in a
+// per-lane waterfall loop (which starves when the sub-partition is busy).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 // arrive on an mbarrier when all prior tcgen05.mma of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {

@@ -31,7 +31,8 @@ __device__ __forceinline__ void wait_mode(int wm, uint64_t *bar, uint32_t parity
     else wait_hint(bar, parity);
 }
 
-__global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out) {
+__global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out, int burn,
+                       int smsp_mask, int PW, int MW, int nowait, int yield_every) {
     const int wm = mode / 10;
     mode %= 10;
     __shared__ __align__(1024) uint8_t tile[16384];
@@ -66,18 +67,52 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out)
                 }
             }
         }
-    } else if (warp == 0 && lane == 0) {
+    } else if (warp != PW && warp != MW && burn && ((smsp_mask >> (warp & 3)) & 1)) {
+        // ALU burner warps (FP32 FMA chains, 8 independent) while the MMA runs
+        float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+              a6 = a0 + 6, a7 = a0 + 7;
+        for (int i = 0; i < iters * burn; ++i) {
+            if (yield_every && (i % yield_every) == 0) asm volatile("nanosleep.u32 0;");
+            a0 = fmaf(a0, 1.0001f, 0.3f); a1 = fmaf(a1, 1.0001f, 0.3f);
+            a2 = fmaf(a2, 1.0001f, 0.3f); a3 = fmaf(a3, 1.0001f, 0.3f);
+            a4 = fmaf(a4, 1.0001f, 0.3f); a5 = fmaf(a5, 1.0001f, 0.3f);
+            a6 = fmaf(a6, 1.0001f, 0.3f); a7 = fmaf(a7, 1.0001f, 0.3f);
+        }
+        if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 0.123f) out[0] = 1;
+    } else if (warp == PW && lane == 0 && !(nowait & 1)) {
         for (int i = 0; i < iters; ++i) {
             const int s = i % stages;
             wait_mode(wm, &empty[s], ((i / stages) & 1) ^ 1);
             mbar_arrive(&full[s]);
         }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == MW && (nowait & 2)) {
+        // whole warp runs the loop; one elected lane issues
         const uint32_t idesc = idesc_f16(128, 128);
         const uint64_t bd = desc_sw128(smem_u32(tile));
         for (int i = 0; i < iters; ++i) {
             const int s = i % stages;
-            wait_mode(wm, &full[s], (i / stages) & 1);
+            if (!(nowait & 1)) wait_mode(wm, &full[s], (i / stages) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                for (int k = 0; k < 12; ++k)
+                    mma_f16_ts(tmem, tmem + 256 + 8 * (k & 3), bd + 2 * (k & 3), idesc, 1);
+                if (!(nowait & 1)) mma_commit(&empty[s]);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) {
+            if (nowait & 1) mma_commit(&empty[(iters - 1) % stages]);
+            if (nowait & 1) wait_mode(wm, &empty[(iters - 1) % stages], 0);
+            else wait_mode(wm, &empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
+            out[blockIdx.x] = clock64() - t0;
+        }
+        __syncwarp();
+    } else if (warp == MW && lane == 0) {
+        const uint32_t idesc = idesc_f16(128, 128);
+        const uint64_t bd = desc_sw128(smem_u32(tile));
+        for (int i = 0; i < iters; ++i) {
+            const int s = i % stages;
+            if (!(nowait & 1)) wait_mode(wm, &full[s], (i / stages) & 1);
             tc_fence_after();
             if (mode == 0) {
                 mbar_arrive(&empty[s]);
@@ -99,12 +134,17 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out)
                 for (int k = 0; k < 12; ++k)
                     mma_f16(tmem, bd + 2 * (k & 3), bd + 2 * (k & 3), idesc, 1);
             }
-            mma_commit(&empty[s]);
+            if (!(nowait & 1)) mma_commit(&empty[s]);
         }
+        if (nowait & 1) mma_commit(&empty[(iters - 1) % stages]);
+        // wait for the last MMAs, then stamp (the burners may run longer)
+        if (nowait & 1) wait_mode(wm, &empty[(iters - 1) % stages], 0);
+        else wait_mode(wm, &empty[(iters - 1) % stages], ((iters - 1) / stages) & 1);
+        out[blockIdx.x] = clock64() - t0;
     }
     __syncthreads();
     const unsigned long long t1 = clock64();
-    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0 && mode >= 5) out[blockIdx.x] = t1 - t0;
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -117,10 +157,15 @@ int main() {
     const char *names[] = {"plain arrive", "commit only", "12 MMA TS + commit", "12 MMA SS + commit",
                            "12 TS hi/lo/lo", "1T arrive", "1T try_wait done", "1T arrive+wait",
                            "12 TS 4hi+8lo", "6 TS N=256"};
-    for (int mode : {1, 2, 4, 8, 9, 3}) {
-        for (int stages : {4}) {
-            const int iters = 2000;
-            k_pipe<<<148, 128>>>(mode, iters, stages, d);
+    for (int mode : {2}) {
+      for (int burn : {64}) {
+       for (int nthr : {512}) {
+        for (int pm : {0x01, 0x10001, 0x20001, 0x40001, 0x80001}) {
+            const int PW = (pm >> 4) & 15, MW = pm & 15, mask = ((pm >> 12) & 15) ? 0xd : 0xf;
+            const int nowait = (pm >> 8) & 3;
+            const int iters = 2000, stages = 4;
+            const int yield_every = pm >> 16;
+            k_pipe<<<148, nthr>>>(mode, iters, stages, d, burn, mask, PW, MW, nowait, yield_every);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
                 printf("error %s\n", cudaGetErrorString(e));
@@ -130,8 +175,10 @@ int main() {
             double avg = 0;
             for (int i = 0; i < 148; ++i) avg += h[i];
             avg /= 148;
-            printf("%-22s wait=%d stages=%d  %8.1f cycles/iter\n", names[mode % 10], mode / 10, stages, avg / iters);
+            printf("%-22s burn=%2d threads=%d mask=%x nowait=%d yield=%d  %8.1f cycles/iter\n", names[mode % 10], burn, nthr, mask, nowait, yield_every, avg / iters);
         }
+       }
+      }
     }
     return 0;
 }

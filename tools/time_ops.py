@@ -26,4 +26,8 @@ for name in ("forward", "adjoint"):
         b.record(); b.synchronize()
         if i >= 3: ts.append(a.elapsed_time(b) * 1e3)
     res[name] = np.median(ts)
-print(f"cfg {cfg} exp={os.environ.get('CSR_EXP','0')} split={op.info()['split_k']} fwd {res['forward']:.1f} us adj {res['adjoint']:.1f} us", flush=True)
+import ctypes
+fm, am, fn, an = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+_native.call("csr_plan_kernel_times", op.plan, ctypes.byref(fm), ctypes.byref(am), ctypes.byref(fn), ctypes.byref(an))
+print(f"cfg {cfg} exp={os.environ.get('CSR_EXP','0')} split={op.info()['split_k']} fwd {res['forward']:.1f} us adj {res['adjoint']:.1f} us"
+      f" | kernels fwd {fm.value*1e3:.1f} adj {am.value*1e3:.1f} us", flush=True)
