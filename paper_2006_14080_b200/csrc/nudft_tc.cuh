@@ -57,7 +57,7 @@ struct TcPlan {
     unsigned long long *probe = nullptr;   // [2][4] live timing slots: forward, adjoint
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags
     int G_ts = 1, ntpg_ts = 1, fts_smem = 0;
-    int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0, adj_cs = 1;
+    int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
@@ -720,9 +720,8 @@ __device__ __forceinline__ void tmem_st_n(uint32_t a, const uint32_t (&r)[16]) {
 struct AdjParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
     TcArgs a;
-    int S, kb_per_split, kb_total, raw_bytes, raw_stage, n_raw, chain;
+    int S, kb_per_split, kb_total, raw_bytes, n_raw, chain;
     int exp_flags;  // profiling experiments: 1 = no generator math, 2 = no MMA
-    int cs;         // cluster size along the (x, c) tiles sharing one B tile
     unsigned long long *trace;
     const float2 *sens;
     float2 *ws;  // [S][T][nx][ny]
@@ -734,18 +733,15 @@ constexpr int ADJ_STAGES = 4;             // B tiles in smem = A stages in TMEM
 constexpr int ADJ_B_TILE = 128 * 128;     // 16 KiB (one of hi / lo)
 constexpr int ADJ_B_STAGE = 2 * ADJ_B_TILE;
 constexpr int ADJ_MAX_RAW = 8;            // generator-input ring depth (max)
-// warps: 0 B-ring TMA, 1 MMA, 2 raw-ring TMA, 3 idle, 4 .. 4+GW-1 generators
-// (GW / 4 per TMEM lane quarter, each writing SPW samples of a K block),
-// then four epilogue warps
+// warps: 0 B-ring TMA, 1 MMA, 2 input-ring TMA, 3 input prep,
+// 4 .. 4+GW-1 generators (GW / 4 per TMEM lane quarter, each writing SPW
+// samples of a K block), then four epilogue warps
 #ifndef ADJ_GW
 #define ADJ_GW 4
 #endif
 // Barrier waits: the long ones (producers, epilogue) sleep on the barrier
 // (ADJ_SLEEP_SLOW), the latency-critical ones (MMA issuer, generators) spin
 // unless ADJ_SLEEP_FAST.
-#ifndef ADJ_MERGED_N256
-#define ADJ_MERGED_N256 1
-#endif
 #ifndef ADJ_SLEEP_SLOW
 #define ADJ_SLEEP_SLOW 1
 #endif
@@ -770,30 +766,43 @@ constexpr int ADJ_SPW = 32 * 4 / ADJ_GW;
 constexpr int ADJ_W_EPI = 4 + ADJ_GW;
 constexpr int ADJ_THREADS = (ADJ_W_EPI + 4) * 32;
 constexpr int ADJ_SUM_LD = 129;                       // padded row (floats)
-constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 running sums [y][lane]
+constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 sums [y][lane]
+static_assert(ADJ_SUM_BYTES <= ADJ_STAGES * ADJ_B_STAGE, "sums reuse the B ring");
+
+// Input-ring stage layout (bytes): P0 rows [32][XS] c64 | d [32][CP] c64 |
+// d' [32][CP][2] c64, d' = sg * ((dr, di), (di, -dr)) so that generator row
+// (x, c, part) gets its two values with two FMUL + two FFMA and no selects.
+__host__ __device__ constexpr int adj_in_stage_bytes(int CP) {
+    return ((32 * (64 / CP) * 8 + 32 * CP * 8 + 32 * CP * 16) + 127) / 128 * 128;
+}
 
 // Adjoint, "A from TMEM" form, one tile x one contiguous k range per CTA.
 // Tile = 128 rows (x, c, part) of the generated operand W' (64 complex
 // (x, c) columns) x 128 pixel rows y; K = 32 samples (64 fp16) per block.
-// The generator warpgroup writes W' straight into tensor memory with
-// tcgen05.st, so shared memory only carries the static factor conj(P1)^T
-// (TMA, 128B swizzle) and the P0 / d inputs of the generator.
+// The generators write W' straight into tensor memory with tcgen05.st, so
+// shared memory only carries the static factor conj(P1)^T (TMA, 128B
+// swizzle) and the P0 / d inputs of the generators.
 //
-// Three rings keep the tensor core fed:
+// Rings:
 //   B ring   (4 smem stages): TMA (warp 0) -> MMA; freed by the MMA commit.
-//   raw ring (n_raw smem stages, deeper): TMA (warp 2) -> generators; freed
-//            as soon as the generators have the values in registers, so the
-//            inputs of block i are resident long before its A stage frees.
+//   in ring  (n_raw smem stages): TMA (warp 2) -> prep (warp 3, scales and
+//            rotates d into d') -> generators; freed as soon as the
+//            generators hold the values in registers.
 //   A ring   (4 TMEM stages): generators -> MMA; freed by the same MMA
 //            commit as the B stage of that block.
-// A generator therefore waits only for the MMA that last used its TMEM
-// stage, not for a TMA round trip behind it.
+// Per K step one N = 256 MMA multiplies A_hi by [B_hi ; B_lo] (one 256-row
+// SW128 tile) into [D_hi | D_lo], and one N = 128 MMA adds A_lo * B_hi to
+// D_lo: 8 MMA instructions per K block.  The single-thread roles share
+// their SM sub-partitions with generator warps, and the warp scheduler
+// favours busy ALU warps, so every generator instruction removed is MMA
+// issue bandwidth regained (measured: tools/pipe_micro.cu).
 //
 // The k range is cut into accumulation chains of <= chain blocks (the
-// tensor core truncates on every fp32 accumulate); the epilogue warpgroup
-// drains each chain into an fp32 running sum in shared memory and frees the
-// accumulator.  After the last chain all warps combine coils and
-// write one split-K partial image.
+// tensor core truncates on every fp32 accumulate); the epilogue warps drain
+// each chain into fp32 running sums held in registers and free the
+// accumulator.  After the last chain the sums go to shared memory
+// (transposed, over the idle B ring) and all warps combine coils into one
+// split-K partial image.
 //   TMEM columns: [0,128) hi*hi accumulator, [128,256) hi*lo + lo*hi
 //   corrections, [256,512) four A stages of (hi 32 | lo 32).
 template <int CP>
@@ -806,16 +815,18 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
     constexpr int XS = 64 / CP;  // x values per tile
+    constexpr int IN_STAGE = adj_in_stage_bytes(CP);
+    constexpr int OFF_D = 32 * XS * 8, OFF_DP = OFF_D + 32 * CP * 8;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    uint8_t *raw_base = smem + ADJ_STAGES * ADJ_B_STAGE;
-    float *sum_s = reinterpret_cast<float *>(raw_base + P.n_raw * P.raw_stage);
-    uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(sum_s) +
-                                                  ADJ_SUM_BYTES);
+    uint8_t *in_base = smem + ADJ_STAGES * ADJ_B_STAGE;
+    float *sum_s = reinterpret_cast<float *>(smem);  // after the main loop
+    uint64_t *full = reinterpret_cast<uint64_t *>(in_base + P.n_raw * IN_STAGE);
     uint64_t *gen = full + ADJ_STAGES;
     uint64_t *empty = gen + ADJ_STAGES;
     uint64_t *rfull = empty + ADJ_STAGES;
-    uint64_t *rempty = rfull + ADJ_MAX_RAW;
+    uint64_t *dfull = rfull + ADJ_MAX_RAW;
+    uint64_t *rempty = dfull + ADJ_MAX_RAW;
     uint64_t *acc_full = rempty + ADJ_MAX_RAW;
     uint64_t *acc_empty = acc_full + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
@@ -845,10 +856,11 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         for (int s = 0; s < ADJ_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&gen[s], ADJ_GW);
-            mbar_init(&empty[s], P.cs);  // every cluster CTA's MMA frees stage s
+            mbar_init(&empty[s], 1);
         }
         for (int r = 0; r < NR; ++r) {
             mbar_init(&rfull[r], 1);
+            mbar_init(&dfull[r], 1);
             mbar_init(&rempty[r], ADJ_GW);
         }
         mbar_init(acc_full, 1);
@@ -858,55 +870,58 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
-    if (P.cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t crank = P.cs > 1 ? cluster_ctarank() : 0;
-    const uint16_t cmask = (uint16_t)((1u << P.cs) - 1);
 
     if (warp == 0) {
         // ---- B ring producer: conj(P1)^T hi / lo tiles
         if (lane == 0) {
             const int brow = t * P.a.nyA + nt * 128;
-            const uint32_t tx = (P.exp_flags & 8) ? 0 : ADJ_B_STAGE;
             for (int i = 0; i < nkb; ++i) {
                 const int kb = kb0 + i;
                 const int s = i % ADJ_STAGES;
                 wait_slow(&empty[s], ((i / ADJ_STAGES) & 1) ^ 1);
                 uint8_t *st = smem + s * ADJ_B_STAGE;
-                mbar_arrive_expect_tx(&full[s], tx);
-                if (P.exp_flags & 8) {
-                } else if (P.cs > 1) {
-                    // this CTA fetches rows [crank*R, (crank+1)*R) of the shared
-                    // B tile and multicasts them to the whole cluster
-                    const int R = 128 / P.cs;
-                    tma_load_2d_mc(st + crank * R * 128, &tmB_hi, &full[s], kb * 64,
-                                   brow + crank * R, cmask);
-                    tma_load_2d_mc(st + ADJ_B_TILE + crank * R * 128, &tmB_lo, &full[s],
-                                   kb * 64, brow + crank * R, cmask);
-                } else {
-                    tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
-                    tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
-                }
+                mbar_arrive_expect_tx(&full[s], ADJ_B_STAGE);
+                tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
+                tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
             }
         }
     } else if (warp == 2) {
-        // ---- raw ring producer: P0 rows of the tile's x values, and d
+        // ---- input ring producer: P0 rows of the tile's x values, and d
         if (lane == 0) {
-            const uint32_t tx = (P.exp_flags & 16) ? 0 : P.raw_bytes;
+            const uint32_t tx = P.raw_bytes;
             for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
                 const int kb = kb0 + i;
                 wait_slow(&rempty[r], rph ^ 1);
-                uint8_t *raw = raw_base + r * P.raw_stage;
+                uint8_t *in = in_base + r * IN_STAGE;
                 mbar_arrive_expect_tx(&rfull[r], tx);
-                if (!(P.exp_flags & 16)) {
-                    tma_load_3d(raw, &tmP0, &rfull[r], mt * XS, kb * 32, t);
-                    tma_load_3d(raw + 32 * XS * 8, &tmKd, &rfull[r], 0, kb * 32, t);
-                }
+                tma_load_3d(in, &tmP0, &rfull[r], mt * XS, kb * 32, t);
+                tma_load_3d(in + OFF_D, &tmKd, &rfull[r], 0, kb * 32, t);
                 if (++r == NR) {
                     r = 0;
                     rph ^= 1;
                 }
+            }
+        }
+    } else if (warp == 3) {
+        // ---- input prep: d' = sg * ((dr, di), (di, -dr)) per (k, c)
+        const float sg = pow2_scale(P.scales[5]);
+        for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
+            wait_slow(&rfull[r], rph);
+            uint8_t *in = in_base + r * IN_STAGE;
+            const float2 *d = reinterpret_cast<const float2 *>(in + OFF_D);
+            float4 *dp = reinterpret_cast<float4 *>(in + OFF_DP);
+#pragma unroll
+            for (int e = lane; e < 32 * CP; e += 32) {
+                const float2 v = d[e];
+                dp[e] = make_float4(sg * v.x, sg * v.y, sg * v.y, -sg * v.x);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dfull[r]);
+            if (++r == NR) {
+                r = 0;
+                rph ^= 1;
             }
         }
     } else if (warp == 1) {
@@ -929,28 +944,18 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * ADJ_B_STAGE);
                     const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
+                    if (!(P.exp_flags & 2)) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t dbh = desc_sw128(st + kk * 32);
-                        const uint64_t dbl = desc_sw128(st + ADJ_B_TILE + kk * 32);
-                        const uint32_t acc = (i != i0) || (kk != 0);
-                        if (P.exp_flags & 2) continue;
-#if ADJ_MERGED_N256
-                        // B' = [hi_B ; lo_B] is one 256-row SW128 tile: a single
-                        // N = 256 MMA writes hi*hi_B to D_hi and hi*lo_B to D_lo
-                        (void)dbl;
-                        mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc256, acc);
-                        mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
-#else
-                        mma_f16_ts(d_hi, a_hi + 8 * kk, dbh, idesc, acc);
-                        mma_f16_ts(d_lo, a_hi + 8 * kk, dbl, idesc, acc);
-                        mma_f16_ts(d_lo, a_lo + 8 * kk, dbh, idesc, 1);
-#endif
+                        for (int kk = 0; kk < 4; ++kk) {
+                            // B' = [hi_B ; lo_B] is one 256-row SW128 tile
+                            const uint64_t db = desc_sw128(st + kk * 32);
+                            const uint32_t acc = (i != i0) || (kk != 0);
+                            mma_f16_ts(d_hi, a_hi + 8 * kk, db, idesc256, acc);
+                            mma_f16_ts(d_lo, a_lo + 8 * kk, db, idesc, 1);
+                        }
                     }
                     // frees B stage s (TMA) and A stage s (generators)
-                    if (P.exp_flags & 32) mbar_arrive(&empty[s]);
-                    else if (P.cs > 1) mma_commit_mc(&empty[s], cmask);
-                    else mma_commit(&empty[s]);
+                    mma_commit(&empty[s]);
                 }
                 mma_commit(acc_full);
             }
@@ -968,13 +973,13 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         const int j = m >> 1, part = m & 1;
         const int xl = j / CP, c = j % CP;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-        const float sg = pow2_scale(P.scales[5]);
         for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
             const int s = i % ADJ_STAGES;
-            wait_fast(&rfull[r], rph);
+            wait_fast(&dfull[r], rph);
             ADJ_TL(1, lane == 0 && warp == 4);
-            const float2 *p0s = reinterpret_cast<const float2 *>(raw_base + r * P.raw_stage);
-            const float2 *ds = p0s + 32 * XS;
+            const uint8_t *in = in_base + r * IN_STAGE;
+            const float2 *p0s = reinterpret_cast<const float2 *>(in);
+            const float2 *dps = reinterpret_cast<const float2 *>(in + OFF_DP) + (c * 2 + part);
             uint32_t hv[ADJ_SPW], lv[ADJ_SPW];
             if (P.exp_flags & 1) {
 #pragma unroll
@@ -983,32 +988,17 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < ADJ_SPW; ++kk) {
                 const int k = h * ADJ_SPW + kk;
-#if ADJ_GEN_VARIANT == 2  // profiling: no shared-memory operands
-                const float2 p = make_float2((float)k, (float)xl);
-                const float2 d = make_float2((float)c, (float)(k + i));
-#else
-                const float2 p = p0s[k * XS + xl], d = ds[k * CP + c];
-#endif
-                const float wr = sg * (p.x * d.x + p.y * d.y);
-                const float wi = sg * (p.x * d.y - p.y * d.x);
+                const float2 p = p0s[k * XS + xl], u = dps[k * CP * 2];
                 // Re row (part 0): (wr, -wi); Im row (part 1): (wi, wr)
-                const float e0 = part ? wi : wr, e1 = part ? wr : -wi;
-#if ADJ_GEN_VARIANT == 1  // profiling: no fp16 conversion
-                hv[kk] = __float_as_uint(e0);
-                lv[kk] = __float_as_uint(e1);
-#elif ADJ_GEN_VARIANT == 3  // profiling: hi conversion only
-                const __half2 hh = __floats2half2_rn(e0, e1);
-                hv[kk] = *reinterpret_cast<const uint32_t *>(&hh);
-                lv[kk] = hv[kk] ^ 0x80008000u;
-#else
+                const float e0 = fmaf(p.x, u.x, p.y * u.y);
+                const float e1 = fmaf(p.y, u.x, -(p.x * u.y));
                 const __half2 hh = __floats2half2_rn(e0, e1);
                 const float2 hf = __half22float2(hh);
                 const __half2 ll = __floats2half2_rn(e0 - hf.x, e1 - hf.y);
                 hv[kk] = *reinterpret_cast<const uint32_t *>(&hh);
                 lv[kk] = *reinterpret_cast<const uint32_t *>(&ll);
-#endif
             }
-            // inputs are in registers: hand the raw stage back to the TMA
+            // inputs are in registers: hand the stage back to the TMA
             __syncwarp();
             if (lane == 0) mbar_arrive(&rempty[r]);
             if (++r == NR) {
@@ -1019,51 +1009,55 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             wait_fast(&empty[s], ((i / ADJ_STAGES) & 1) ^ 1);
             ADJ_TL(2, lane == 0 && warp == 4);
             tc_fence_after();
-            if (!(P.exp_flags & 4)) {
-                const uint32_t col = lane_base + 256 + 64 * s + h * ADJ_SPW;
-                tmem_st_n(col, hv);
-                tmem_st_n(col + 32, lv);
-                tmem_st_wait();
-            }
+            const uint32_t col = lane_base + 256 + 64 * s + h * ADJ_SPW;
+            tmem_st_n(col, hv);
+            tmem_st_n(col + 32, lv);
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[s]);
             ADJ_TL(3, lane == 0 && warp == 4);
         }
-    } else if (warp >= ADJ_W_EPI) {
-        // ---- epilogue warpgroup: drain every chain into the running sums
+    }
+    float sum[128];  // epilogue warps: running sums of row m over the 128 y
+    if (warp >= ADJ_W_EPI) {
+        // ---- epilogue: drain every chain into the register sums
         const int q = warp & 3;
-        const int m = q * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int y = 0; y < 128; ++y) sum[y] = 0.f;
         for (int ch = 0; ch < nchain; ++ch) {
             wait_slow(acc_full, ch & 1);
             tc_fence_after();
-#pragma unroll 1
-            for (int cb = 0; cb < 4; ++cb) {
-                uint32_t rh[32], rl[32];
-                tmem_ld32(lane_base + cb * 32, rh);
-                tmem_ld32(lane_base + 128 + cb * 32, rl);
+#pragma unroll
+            for (int cb = 0; cb < 8; ++cb) {
+                uint32_t rh[16], rl[16];
+                tmem_ld16(lane_base + cb * 16, rh);
+                tmem_ld16(lane_base + 128 + cb * 16, rl);
                 tmem_ld_wait();
-                if (cb == 3) {  // accumulator fully read: let the MMA go on
+                if (cb == 7) {  // accumulator fully read: let the MMA go on
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty);
                 }
 #pragma unroll
-                for (int yy = 0; yy < 32; ++yy) {
-                    const float v = __uint_as_float(rh[yy]) + __uint_as_float(rl[yy]);
-                    float *dst = sum_s + (cb * 32 + yy) * ADJ_SUM_LD + m;
-                    *dst = ch ? *dst + v : v;
-                }
+                for (int yy = 0; yy < 16; ++yy)
+                    sum[cb * 16 + yy] += __uint_as_float(rh[yy]) + __uint_as_float(rl[yy]);
             }
         }
+    }
+    __syncthreads();  // all MMAs and TMA loads are done: the B ring is free
+    if (warp >= ADJ_W_EPI) {
+        const int m = (warp & 3) * 32 + lane;
+#pragma unroll
+        for (int y = 0; y < 128; ++y) sum_s[y * ADJ_SUM_LD + m] = sum[y];
     }
     __syncthreads();
     // ---- combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y), all
     // warps: thread e handles pixel row y = e % 128 for the x values
-    // xq = e / 128 (mod warps / 4) of the tile, reading the transposed sums (padded
-    // rows: conflict-free) and the coil maps with y-coalesced loads
-    if (!(P.exp_flags & 64)) {
+    // xq = e / 128 (mod warps / 4) of the tile, reading the transposed sums
+    // (padded rows: conflict-free) and the coil maps with y-coalesced loads
+    {
         const float inv = 1.f / pow2_scale(P.scales[5]);
         const int e = threadIdx.x & 127, grp = threadIdx.x >> 7;
         const int y = nt * 128 + e;
@@ -1090,7 +1084,6 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             }
         }
     }
-    if (P.cs > 1) cluster_sync();  // no CTA leaves while peers may still signal it
     __syncthreads();
     probe_exit(P.probe);
     if (warp == 1) {
@@ -1244,16 +1237,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
     tc.split = S;
     tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
-    // clusters of CTAs that share one B tile (same frame, split, y tile)
-    tc.adj_cs = 1;  // multicast measured no faster (L2 dedups the shared B tile)
-    if (const char *e = getenv("CSR_ADJ_CLUSTER")) {
-        int v = atoi(e);
-        if ((v == 1 || v == 2 || v == 4) && tc.mt_a % v == 0) tc.adj_cs = v;
-    }
-    tc.adj_stage = (tc.raw_bytes + 127) / 128 * 128;  // raw ring stage
+    tc.adj_stage = adj_in_stage_bytes(Cp);  // input ring stage
     tc.fwd_smem = TC_STAGES * TC_FWD_OPS + 1024 + 256;
     {
-        const int fixed = ADJ_STAGES * ADJ_B_STAGE + ADJ_SUM_BYTES + 1024 + 512;
+        const int fixed = ADJ_STAGES * ADJ_B_STAGE + 1024 + 512;
         tc.adj_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
         if (const char *e = getenv("CSR_ADJ_NRAW"))
             tc.adj_nraw = std::max(1, std::min(tc.adj_nraw, atoi(e)));
@@ -1303,8 +1290,8 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_xb128_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
               tmap_f16_2d(&tc.tm_xb128_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
-              tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
-              tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128 / tc.adj_cs) &&
+              tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
+              tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
               tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
     if (!ok) return 0;  // descriptor encode unavailable: SIMT path
@@ -1421,12 +1408,10 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.kb_per_split = tc.kb_per_split;
     P.chain = TC_MAX_CHAIN;
     P.exp_flags = tc.aexp;
-    P.cs = tc.adj_cs;
     P.trace = tc.trace;
     P.probe = tc.probe ? tc.probe + 4 : nullptr;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
-    P.raw_stage = tc.adj_stage;
     P.n_raw = tc.adj_nraw;
     P.sens = tc.sens;
     P.ws = ws;
@@ -1438,13 +1423,6 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     cfg.blockDim = dim3(ADJ_THREADS);
     cfg.dynamicSmemBytes = tc.adj_smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = tc.adj_cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
     cudaError_t e;
     switch (tc.Cp) {
         case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
