@@ -285,6 +285,14 @@ def run_ours(args, cfg, world, rank, local):
                  ctypes.byref(fn), ctypes.byref(an))
     kt = {"forward": fm.value, "adjoint": am.value}
     kn = {"forward": fn.value, "adjoint": an.value}
+    breakdown = {}
+    for slot, name in enumerate(["forward", "adjoint", "admm_mu", "admm_rhs", "operand_prep",
+                                 "cg_tail", "admm_post"]):
+        ms_, n_ = ctypes.c_double(), ctypes.c_int64()
+        _native.call("csr_plan_probe", op.plan, slot, ctypes.byref(ms_), ctypes.byref(n_))
+        if n_.value:
+            breakdown[name] = {"ms_per_launch": ms_.value,
+                               "launches_per_step": n_.value / args.steps}
     kt_cold = time_kernels(op, prob)
     flops_launch = 8.0 * op.n_coils * op.m_per_frame * op.nx * op.ny * op.n_frames
     pk, src = peaks()
@@ -299,7 +307,9 @@ def run_ours(args, cfg, world, rank, local):
                 "tensor_flops_per_launch": 3 * flops_launch,
                 "ms_per_launch": kt, "launches_timed": kn,
                 "ms_per_launch_cold": kt_cold,
-                "share_of_step": {k: kn[k] / args.steps * v / step_ms for k, v in kt.items()}}
+                "share_of_step": {k: kn[k] / args.steps * v / step_ms for k, v in kt.items()},
+                "step_breakdown_ms": {k: v["ms_per_launch"] * v["launches_per_step"]
+                                      for k, v in breakdown.items()}}
 
     # e2e through the public API with pinned host buffers
     e2e = None
@@ -307,7 +317,7 @@ def run_ours(args, cfg, world, rank, local):
     data_p, sens_p = pinned(prob.data), pinned(prob.sens)
     ds_p = P.KSpaceDataset(data_p, traj, n_frames=prob.n_frames)
     e2e_times = []
-    for i in range(4):
+    for i in range(0 if args.no_e2e else 4):
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -317,13 +327,15 @@ def run_ours(args, cfg, world, rank, local):
         dt = time.perf_counter() - t0
         if i > 0:
             e2e_times.append(max_over_ranks(dt, world))
-    e2e = {"value": n_e2e / float(np.median(e2e_times)), "unit": "iter/s",
-           "h2d_bytes_per_step": int(data_p.nbytes // world + sens_p.nbytes // world +
-                                     prob.coords.nbytes),
-           "d2h_bytes_per_step": int(img.nbytes),
-           "step": f"one admm_reconstruct call ({n_e2e} ADMM iterations, host in/out; "
-                   f"plan build + factor generation included), median of 3 after 1 warm-up",
-           "ms_per_call": [1e3 * t for t in e2e_times]}
+    if e2e_times:
+        e2e = {"value": n_e2e / float(np.median(e2e_times)), "unit": "iter/s",
+               "h2d_bytes_per_step": int(data_p.nbytes // world + sens_p.nbytes // world +
+                                         prob.coords.nbytes),
+               "d2h_bytes_per_step": int(img.nbytes),
+               "step": f"one admm_reconstruct call ({n_e2e} ADMM iterations, host in/out; "
+                       f"plan build + factor generation included), median of 3 after 1 "
+                       f"warm-up",
+               "ms_per_call": [1e3 * t for t in e2e_times]}
 
     out = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
@@ -353,6 +365,7 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="profiling: skip the e2e leg")
     args = ap.parse_args()
     rank, world, local = dist_setup(args.gpus)
     if args.impl == "reference":

@@ -176,6 +176,11 @@ int csr_plan_set_timing(csr_plan *plan, void *flush_buf, int64_t flush_bytes,
 int csr_plan_kernel_times(csr_plan *plan, double *fwd_ms, double *adj_ms,
                           int64_t *n_fwd, int64_t *n_adj);
 
+/* Benchmark: the same live timing for one kernel slot of the iteration:
+ * 0 forward GEMM, 1 adjoint GEMM, 2 mu, 3 rhs, 4 operand prep, 5 fused CG
+ * tail, 6 ADMM post-update. */
+int csr_plan_probe(csr_plan *plan, int32_t slot, double *ms, int64_t *n);
+
 /* adjoint_reconstruct (solver.py:363-406): image = allreduce(F^H d). */
 int csr_adjoint_reconstruct(csr_plan *plan, const void *kdata, void *image,
                             void *stream);

@@ -1,0 +1,273 @@
+// Fused CG tail (single rank, tensor-core operator): one cooperative kernel
+// per CG iteration replaces k_cg_ad + k_cg_xr + k_cg_d + the next forward's
+// k_tc_prep_x (solver.py:111-122):
+//
+//   phase A  Ad = sum_s ws[s] + (beta/2) Theta^H Theta d ;  <d, Ad>
+//   barrier  alpha = tau / <d, Ad>                  (every block, same order)
+//   phase B  x += alpha d ; r -= alpha Ad ;  ||r||^2, max|r|
+//   barrier  beta = tau'/tau, CG bookkeeping (fin_xr)
+//   phase C  d = r + beta d, written both as c64 and as the next forward's
+//            fp16 hi/lo operand X = split(sigma_x * s_c * d)
+//
+// The scalars are reduced deterministically: each block leaves its fp64
+// partial sums in `part`, and after the grid barrier every block sums all
+// of them in block order, so all blocks hold bit-identical alpha / beta
+// without a second round trip.  sigma_x needs a bound on max|d| before d
+// exists; max|r| + |beta| * bound(d_old) is one (component-wise), and the
+// bound actually used is left in scales[6] for the forward's epilogue.
+#pragma once
+
+#include "elementwise.cuh"
+#include "nudft_tc.cuh"
+
+namespace csr {
+
+struct CgTailArgs {
+    Geom g;
+    AdmmBufs b;
+    const float2 *ws;  // split-K partials (coils combined)
+    int S;
+    TcArgs a;          // forward operand geometry
+    const float2 *sens;
+    __half *xb_hi, *xb_lo;
+    float *scales;     // [4] max|s|, [5] k-space max (reset), [6] bound on max|d|
+    double *part;      // [3][grid] fp64 partials
+    unsigned *bar;     // [2] grid barrier: arrivals, generation
+    unsigned long long *probe;  // live timing slot or null
+    unsigned long long *stamps; // debug: phase timestamps of block 0 (CSR_TRACE)
+};
+
+// Sense-reversing grid barrier; the kernel is launched cooperatively, so all
+// blocks are co-resident.
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// block sum of NV doubles into part[i * grid + block]
+template <int NV>
+__device__ __forceinline__ void block_partials(double (&v)[NV], double *part) {
+    __shared__ double sh[NV][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double w = warp_sum(v[i]);
+        if (lane == 0) sh[i][warp] = w;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double w = lane < (int)(blockDim.x >> 5) ? sh[i][lane] : 0.0;
+            w = warp_sum(w);
+            if (lane == 0) part[(size_t)i * gridDim.x + blockIdx.x] = w;
+        }
+    }
+}
+
+// every block: tot[i] = sum over blocks of part[i][*] in block order
+template <int NV>
+__device__ __forceinline__ void all_totals(const double *part, double (&tot)[NV]) {
+    __shared__ double res[NV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double w = 0.0;
+            for (unsigned b = lane; b < gridDim.x; b += 32)
+                w += __ldcg(part + (size_t)i * gridDim.x + b);
+            w = warp_sum(w);
+            if (lane == 0) res[i] = w;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tot[i] = res[i];
+}
+
+#define TAIL_STAMP(i) \
+    if (A.stamps && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
+    A.stamps[(blockIdx.x ? 16 : 0) + (i)] = gtimer()
+__global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
+    pdl_enter();
+    const Geom &g = A.g;
+    const AdmmBufs &b = A.b;
+    DevScalars *s = b.s;
+    if (!s->cg_active) return;  // uniform: every block reads the same flag
+    probe_enter(A.probe);
+    TAIL_STAMP(0);
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    // everything block 0 rewrites below is read before the first barrier
+    const float dbound_old = A.scales[6];
+    const double tau = s->tau, atol2 = s->atol2;
+    const int cg_iter = s->cg_iter + 1, cg_max = s->cg_max, cur = s->cur;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+
+    // ---- phase A: Ad and <d, Ad>
+    {
+        ThetaOf th{b.d, g, nullptr, nullptr};
+        double v[2] = {0.0, 0.0};
+        for (int64_t i = i0; i < g.n; i += stride) {
+            int t, xx, y;
+            unflat(g, i, t, xx, y);
+            const float2 f = coil_combine(A.ws, nullptr, A.S, g.T, 1, nxy, t, i - t * nxy);
+            const float2 l = theta_adj_at(th, g, t, xx, y);
+            const float2 a = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+            b.ad[i] = a;
+            const float2 d = b.d[i];
+            v[0] += (double)d.x * a.x + (double)d.y * a.y;
+            v[1] += (double)d.x * a.y - (double)d.y * a.x;
+        }
+        block_partials<2>(v, A.part);
+    }
+    TAIL_STAMP(1);
+    grid_barrier(A.bar);
+    double dad[2];
+    TAIL_STAMP(2);
+    all_totals<2>(A.part, dad);
+    TAIL_STAMP(3);
+    // fin_ad (solver.py:114): alpha = tau / <d, Ad>
+    const double den = dad[0] * dad[0] + dad[1] * dad[1];
+    const double al_re = tau * dad[0] / den, al_im = -tau * dad[1] / den;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s->alpha_re = al_re;
+        s->alpha_im = al_im;
+    }
+
+    // ---- phase B: x, r and ||r||^2, max|r|
+    {
+        float2 *x = b.rho[cur ^ 1];
+        const float2 al = make_float2((float)al_re, (float)al_im);
+        const float2 nal = make_float2(-al.x, -al.y);
+        double v[1] = {0.0};
+        float rmax = 0.f;
+        for (int64_t i = i0; i < g.n; i += stride) {
+            x[i] = cadd(x[i], cmul(al, b.d[i]));
+            const float2 r = cadd(b.r[i], cmul(nal, b.ad[i]));
+            b.r[i] = r;
+            v[0] += (double)r.x * r.x + (double)r.y * r.y;
+            rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
+        }
+        // slot 2: ||r||^2 partials; slot 3: max|r| partials
+        __shared__ float shm[32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        if (lane == 0) shm[warp] = rmax;
+        block_partials<1>(v, A.part + 2 * (size_t)gridDim.x);  // syncs the block
+        if (warp == 0) {
+            float w = lane < (int)(blockDim.x >> 5) ? shm[lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+            if (lane == 0) A.part[3 * (size_t)gridDim.x + blockIdx.x] = w;
+        }
+    }
+    TAIL_STAMP(4);
+    grid_barrier(A.bar);
+    double tn;
+    TAIL_STAMP(5);
+    float rmax_all;
+    {
+        __shared__ double res_tn;
+        __shared__ float res_rm;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (warp == 0) {
+            double w = 0.0;
+            float m = 0.f;
+            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
+                w += __ldcg(A.part + 2 * (size_t)gridDim.x + bb);
+                m = fmaxf(m, (float)__ldcg(A.part + 3 * (size_t)gridDim.x + bb));
+            }
+            w = warp_sum(w);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) {
+                res_tn = w;
+                res_rm = m;
+            }
+        }
+        __syncthreads();
+        tn = res_tn;
+        rmax_all = res_rm;
+    }
+    TAIL_STAMP(6);
+    // fin_xr (solver.py:116-122), computed identically by every block
+    const bool finite = isfinite(tn);
+    const double be_d = finite ? tn / tau : 0.0;
+    const bool go_on = finite && cg_iter < cg_max && tn > atol2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (!finite) {
+            s->error = 1;
+            s->admm_active = 0;
+        } else {
+            s->beta_cg = be_d;
+        }
+        s->tau = tn;
+        s->cg_iter = cg_iter;
+        s->cg_active = go_on ? 1 : 0;
+    }
+    if (!go_on) {  // the last iteration leaves d as it is (k_cg_d gate)
+        probe_exit(A.probe);
+        return;
+    }
+
+    // ---- phase C: d = r + beta d, and the forward operand of the new d
+    const float be = (float)be_d;
+    const float dbound = rmax_all + fabsf(be) * dbound_old;
+    const float sg = pow2_scale(2.f * A.scales[4] * dbound);
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.scales[5] = 0.f;  // forward atomicMax
+    const TcArgs &a = A.a;
+    const int hy = a.Kf / 2;
+    uint32_t *H = reinterpret_cast<uint32_t *>(A.xb_hi);
+    uint32_t *L = reinterpret_cast<uint32_t *>(A.xb_lo);
+    for (int64_t i = i0; i < g.n; i += stride) {
+        const float2 d = b.d[i], r = b.r[i];
+        const float2 nd = make_float2(r.x + be * d.x, r.y + be * d.y);
+        b.d[i] = nd;
+        int t, xx, y;
+        unflat(g, i, t, xx, y);
+        const int64_t p = (int64_t)xx * g.ny + y;
+        for (int c0 = 0; c0 < a.C; c0 += 8) {
+            float2 sv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                sv[j] = c0 + j < a.C ? A.sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j;
+                if (c >= a.C) break;
+                float2 v = cmul(sv[j], nd);
+                v.x *= sg;
+                v.y *= sg;
+                __half rh, rl, ih, il;
+                split16(v.x, rh, rl);
+                split16(v.y, ih, il);
+                const int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)xx * a.Cp + c);
+                const int64_t e = row * hy + y, e1 = e + hy;
+                H[e] = pack2(rh, hneg(ih));
+                L[e] = pack2(rl, hneg(il));
+                H[e1] = pack2(ih, rh);
+                L[e1] = pack2(il, rl);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
+    TAIL_STAMP(7);
+    probe_exit(A.probe);
+}
+
+}  // namespace csr

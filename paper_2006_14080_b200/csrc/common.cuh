@@ -4,8 +4,77 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace csr {
+
+// Programmatic dependent launch.  Every kernel of the solver loop starts
+// with pdl_wait() (griddepcontrol.wait: returns once the preceding kernel has
+// completed and its writes are visible; a no-op for an ordinary launch) and
+// then lets its own dependent launch (griddepcontrol.launch_dependents), so
+// inside the captured iteration graph a kernel's CTAs are resident and
+// waiting when its predecessor drains instead of paying the launch gap.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// live-timing slots (csr_plan_probe)
+enum ProbeSlot { PROBE_FWD = 0, PROBE_ADJ, PROBE_MU, PROBE_RHS, PROBE_PREP, PROBE_TAIL,
+                 PROBE_POST, PROBE_SNAP, PROBE_SLOTS };
+
+// Live kernel timing (bench.py's roofline) without perturbing the launch
+// stream: pr = {~first CTA start, CTA ticket, sum of durations (ns),
+// launches}.  Every CTA stamps its start; the last CTA to finish adds
+// (its end - first start) and re-arms the slot for the next launch.
+__device__ __forceinline__ void probe_enter(unsigned long long *pr) {
+    if (pr && threadIdx.x == 0) atomicMax(&pr[0], ~(unsigned long long)gtimer());
+}
+__device__ __forceinline__ void probe_exit(unsigned long long *pr) {
+    if (!pr || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned long long n = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(&pr[1], 1ull) == n - 1) {
+        const unsigned long long t1 = gtimer();
+        const unsigned long long t0 = ~atomicExch(&pr[0], 0ull);
+        atomicAdd(&pr[2], t1 - t0);
+        atomicAdd(&pr[3], 1ull);
+        atomicExch(&pr[1], 0ull);
+    }
+}
+
+inline bool pdl_enabled() {
+    static const bool on = getenv("CSR_NO_PDL") == nullptr;
+    return on;
+}
+
+// kernel<<<grid, block, smem, st>>>(args...) with the programmatic-
+// serialization attribute (the kernel must begin with pdl_enter())
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 __host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

@@ -18,6 +18,7 @@
 #include "elementwise.cuh"
 #include "nudft_simt.cuh"
 #include "nudft_tc.cuh"
+#include "cg_tail.cuh"
 
 using namespace csr;
 
@@ -98,6 +99,8 @@ struct csr_plan {
     float2 *hprev = nullptr, *hnext = nullptr, *sfirst = nullptr, *slast = nullptr;
     double *loc = nullptr;
     double *mpart = nullptr;  // grid-max partials of the d producers
+    double *tail_part = nullptr;  // fused CG tail: [4][<= 1024 blocks] partials
+    int tail_blocks = 0;          // its cooperative grid (0: not computed yet)
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
     int64_t flush_bytes = 0;
@@ -147,16 +150,16 @@ int check_device(int dev) {
 // in the plan's internal k-space buffer (what run_adjoint_partials(nullptr)
 // consumes); otherwise it is written as (T*M, C).
 int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
-                const int *gate, bool in_loop = false) {
+                const int *gate, bool in_loop = false, bool x_ready = false) {
     if (p->tc.enabled) {
-        if (tc_forward(p->tc, x, out, st, gate, in_loop))
+        if (tc_forward(p->tc, x, out, st, gate, in_loop, x_ready))
             return fail(CSR_ERR_CUDA, "tc forward launch");
-        g_launches.fetch_add(tc_forward_launches(p->tc, in_loop, out != nullptr),
+        g_launches.fetch_add(tc_forward_launches(p->tc, in_loop, out != nullptr, x_ready),
                              std::memory_order_relaxed);
         return CSR_OK;
     }
     dim3 grid((unsigned)((p->M + ST - 1) / ST), (unsigned)p->C, (unsigned)p->T);
-    k_forward_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, p->sens, x, out ? out : p->kd,
+    launch(k_forward_simt, grid, 256, 0, st, p->P0, p->P1, p->sens, x, out ? out : p->kd,
                                          (int)p->M, p->nx, p->ny, p->C, gate);
     LAUNCHED();
     return CSR_OK;
@@ -173,7 +176,7 @@ int run_adjoint_partials(csr_plan *p, const float2 *kd, cudaStream_t st,
     }
     int tiles = ((p->nx + ST - 1) / ST) * ((p->ny + ST - 1) / ST);
     dim3 grid((unsigned)tiles, (unsigned)p->C, (unsigned)(p->T * p->S));
-    k_adjoint_simt<<<grid, 256, 0, st>>>(p->P0, p->P1, kd ? kd : p->kd, p->ws, (int)p->M,
+    launch(k_adjoint_simt, grid, 256, 0, st, p->P0, p->P1, kd ? kd : p->kd, p->ws, (int)p->M,
                                          p->nx, p->ny, p->C, p->T, p->kchunk, gate);
     LAUNCHED();
     return CSR_OK;
@@ -236,7 +239,7 @@ int scalar_sync(csr_plan *p, const AdmmBufs &b, int op, int off, int cnt, cudaSt
     if (nranks(p) > 1)
         NC(ncclAllReduce(p->loc + off, p->loc + off, (size_t)cnt, ncclDouble, ncclSum,
                          p->comm->comm, st));
-    k_finalize<<<1, 1, 0, st>>>(b, op);
+    launch(k_finalize, 1, 1, 0, st, b, op);
     LAUNCHED();
     ++*nk;
     return CSR_OK;
@@ -271,58 +274,129 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
     b.tcs = p->tc.enabled ? p->tc.scales : nullptr;
     b.mpart = p->mpart;
     b.mtick = p->tickets + 4;
+    b.probe = p->tc.probe;
     return b;
 }
 
 // One ADMM iteration as a fixed kernel sequence (captured as a graph).
+// The fused CG tail (cg_tail.cuh) on a single rank with the tensor-core
+// operator; multi-rank and SIMT runs keep the separate kernels.
+int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
+    if (!p->tail_blocks) {
+        int per_sm = 0, sms = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail, TPB, 0));
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev));
+        int64_t want = reduce_blocks(p->g.n * (p->C > 1 ? 2 : 1), TPB);
+        if (const char *e = getenv("CSR_TAIL_BLOCKS")) want = atoi(e);
+        p->tail_blocks = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)per_sm * sms, 1024}));
+    }
+    CgTailArgs A;
+    A.g = p->g;
+    A.b = b;
+    A.ws = p->ws;
+    A.S = p->S;
+    A.a = tc_args(p->tc);
+    A.sens = p->sens;
+    A.xb_hi = p->tc.xb_hi;
+    A.xb_lo = p->tc.xb_lo;
+    A.scales = p->tc.scales;
+    A.part = p->tail_part;
+    A.bar = p->tickets + 8;
+    A.probe = p->tc.probe ? p->tc.probe + 4 * PROBE_TAIL : nullptr;
+    A.stamps = p->tc.trace ? p->tc.trace + 100000 : nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p->tail_blocks);
+    cfg.blockDim = dim3(TPB);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, k_cg_tail, A));
+    LAUNCHED();
+    return CSR_OK;
+}
+
+inline bool use_cg_tail(const csr_plan *p) {
+    static const bool off = getenv("CSR_NO_CG_TAIL") != nullptr;
+    return !off && p->tc.enabled && !p->frame_mode && !(p->comm && p->comm->nranks > 1);
+}
+
 int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
                            cudaStream_t st, int *nk) {
     const Geom g = p->g;
     const int eb = ew_blocks(g.n), ebD = ew_blocks(g.n * g.D);
     const int ebf = ew_blocks((int64_t)g.nx * g.ny);
     const bool fm = p->frame_mode;
+    // profiling only (CSR_DBG_SKIP bits, results meaningless): 2 = CG tail,
+    // 4 = forward, 8 = adjoint, 16 mu, 32 rhs, 64 post, 128 snapshot;
+    // 256 = run prep_x before the first forward
+    static const int skip = getenv("CSR_DBG_SKIP") ? atoi(getenv("CSR_DBG_SKIP")) : 0;
     int k = 0;
+    if (skip) {
+        if (!(skip & 16)) launch(k_admm_mu, ebD, TPB, 0, st, g, b);
+        if (!(skip & 32)) launch(k_admm_rhs, eb, TPB, 0, st, g, b);
+        for (int it = 0; it < cg_max; ++it) {
+            const bool prep = it == 0 && (skip & 256);
+            if (!(skip & 4)) TRY(run_forward(p, p->d, nullptr, st, nullptr, true, !prep));
+            if (!(skip & 8)) TRY(run_adjoint_partials(p, nullptr, st, nullptr));
+            if (!(skip & 2)) TRY(launch_cg_tail(p, b, st));
+        }
+        if (!(skip & 64)) launch(k_admm_post, ebD, TPB, 0, st, g, b);
+        if (!(skip & 128)) launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]);
+        *nk = 0;
+        return CSR_OK;
+    }
     if (fm) {  // rho halos for theta(rho)
-        k_stage_frames<<<ebf, TPB, 0, st>>>(b, g, 0, p->sfirst, p->slast); LAUNCHED(); ++k;
+        launch(k_stage_frames, ebf, TPB, 0, st, b, g, 0, p->sfirst, p->slast); LAUNCHED(); ++k;
         TRY(halo_exchange(p, p->sfirst, p->slast, st));
     }
-    k_admm_mu<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    launch(k_admm_mu, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
     if (fm) TRY(halo_exchange(p, p->sfirst, p->sfirst, st));  // next rank's (mu-eta)_t[0]
-    k_admm_rhs<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    launch(k_admm_rhs, eb, TPB, 0, st, g, b); LAUNCHED(); ++k;
     TRY(scalar_sync(p, b, FIN_RHS, 0, 1, st, &k));
     const int *gate = &p->sc->cg_active;
     const bool coil_multi = !fm && p->comm && p->comm->nranks > 1;
     const int64_t nf = (int64_t)g.nx * g.ny;
+    const bool tail = use_cg_tail(p);
     for (int it = 0; it < cg_max; ++it) {
         if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
-        TRY(run_forward(p, p->d, nullptr, st, gate, true));
-        k += p->tc.enabled ? tc_forward_launches(p->tc, true, false) : 1;
+        const bool x_ready = tail && it > 0;  // the previous tail wrote X
+        TRY(run_forward(p, p->d, nullptr, st, gate, true, x_ready));
+        k += p->tc.enabled ? tc_forward_launches(p->tc, true, false, x_ready) : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.adj_launches : 1;
+        if (tail) {
+            TRY(launch_cg_tail(p, b, st));
+            ++k;
+            continue;
+        }
         if (coil_multi) {
-            k_cg_fhf<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
+            launch(k_cg_fhf, eb, TPB, 0, st, g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
             TRY(allreduce(p, p->fhf, g.n, st));
-            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, nullptr, p->sens, p->S, p->C); LAUNCHED(); ++k;
+            launch(k_cg_ad, eb, TPB, 0, st, g, b, nullptr, p->sens, p->S, p->C); LAUNCHED(); ++k;
         } else {
-            k_cg_ad<<<eb, TPB, 0, st>>>(g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
+            launch(k_cg_ad, eb, TPB, 0, st, g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
         }
         TRY(scalar_sync(p, b, FIN_AD, 1, 2, st, &k));
-        k_cg_xr<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+        launch(k_cg_xr, eb, TPB, 0, st, g, b); LAUNCHED(); ++k;
         TRY(scalar_sync(p, b, FIN_XR, 3, 1, st, &k));
-        k_cg_d<<<eb, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+        launch(k_cg_d, eb, TPB, 0, st, g, b); LAUNCHED(); ++k;
     }
     if (fm) {  // halos of the new image for theta(rho+)
-        k_stage_frames<<<ebf, TPB, 0, st>>>(b, g, 1, p->sfirst, p->slast); LAUNCHED(); ++k;
+        launch(k_stage_frames, ebf, TPB, 0, st, b, g, 1, p->sfirst, p->slast); LAUNCHED(); ++k;
         TRY(halo_exchange(p, p->sfirst, p->slast, st));
     }
-    k_admm_post<<<ebD, TPB, 0, st>>>(g, b); LAUNCHED(); ++k;
+    launch(k_admm_post, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
     TRY(scalar_sync(p, b, FIN_POST, 4, 2, st, &k));
-    k_snapshot<<<eb, TPB, 0, st>>>(g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
+    launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
     *nk = k;
     return CSR_OK;
 }
 
 __global__ void k_flush(uint4 *buf, int64_t n, unsigned v) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         buf[i] = make_uint4(v, v, v, v);
@@ -330,6 +404,7 @@ __global__ void k_flush(uint4 *buf, int64_t n, unsigned v) {
 
 __global__ void k_copy_cur(int64_t n, const DevScalars *s, const float2 *r0,
                            const float2 *r1, float2 *out) {
+    pdl_enter();
     const float2 *src = s->cur ? r1 : r0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -395,7 +470,7 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     {
         int64_t total = rows * (p->nx + p->ny);
         int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-        k_factors<<<blocks, 256, 0, st>>>(dcoords, rows, p->nx, p->ny, p->P0, p->P1);
+        launch(k_factors, blocks, 256, 0, st, dcoords, rows, p->nx, p->ny, p->P0, p->P1);
         g_launches.fetch_add(1);
         if (cudaGetLastError() != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "k_factors launch"));
     }
@@ -443,9 +518,10 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         if ((rc = dalloc(p, &p->sfirst, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
         if ((rc = dalloc(p, &p->slast, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
     }
-    if ((rc = dalloc(p, &p->tickets, 8, &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->tail_part, (size_t)(4 * 1024), &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->tickets, 16, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->sc, 1, &p->ws_bytes))) return cleanup(rc);
-    if (cudaMemsetAsync(p->tickets, 0, 8 * sizeof(unsigned), st) != cudaSuccess)
+    if (cudaMemsetAsync(p->tickets, 0, 16 * sizeof(unsigned), st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, "memset"));
     if (cudaStreamSynchronize(st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, std::string("plan build: ") +
@@ -519,7 +595,7 @@ int csr_theta(int32_t T, int32_t nx, int32_t ny, const void *img, void *diffs,
               void *stream) {
     if (T < 1 || nx < 1 || ny < 1) return fail(CSR_ERR_SHAPE, "bad geometry");
     Geom g = make_geom(T, nx, ny);
-    k_theta<<<ew_blocks(g.n * g.D), TPB, 0, (cudaStream_t)stream>>>(
+    launch(k_theta, ew_blocks(g.n * g.D), TPB, 0, (cudaStream_t)stream, 
         g, (const float2 *)img, (float2 *)diffs);
     LAUNCHED();
     return CSR_OK;
@@ -529,7 +605,7 @@ int csr_theta_adjoint(int32_t T, int32_t nx, int32_t ny, const void *diffs,
                       void *img, void *stream) {
     if (T < 1 || nx < 1 || ny < 1) return fail(CSR_ERR_SHAPE, "bad geometry");
     Geom g = make_geom(T, nx, ny);
-    k_theta_adj<<<ew_blocks(g.n), TPB, 0, (cudaStream_t)stream>>>(
+    launch(k_theta_adj, ew_blocks(g.n), TPB, 0, (cudaStream_t)stream, 
         g, (const float2 *)diffs, (float2 *)img);
     LAUNCHED();
     return CSR_OK;
@@ -538,7 +614,7 @@ int csr_theta_adjoint(int32_t T, int32_t nx, int32_t ny, const void *diffs,
 int csr_soft_threshold(const void *z, int64_t n, float t, void *out, void *stream) {
     if (!(t >= 0.f)) return fail(CSR_ERR_ARG, "threshold must be >= 0");
     if (n <= 0) return CSR_OK;
-    k_soft<<<ew_blocks(n), TPB, 0, (cudaStream_t)stream>>>((const float2 *)z, n, t,
+    launch(k_soft, ew_blocks(n), TPB, 0, (cudaStream_t)stream, (const float2 *)z, n, t,
                                                            (float2 *)out);
     LAUNCHED();
     return CSR_OK;
@@ -557,7 +633,7 @@ int csr_hermitian_dot(const void *a, const void *b, int64_t n, double *out,
     CU(cudaMallocAsync(&scratch, bytes, st));
     unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * 2 * sizeof(double));
     CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
-    k_hdot<<<blocks, TPB, 0, st>>>((const float2 *)a, (const float2 *)b, n,
+    launch(k_hdot, blocks, TPB, 0, st, (const float2 *)a, (const float2 *)b, n,
                                    (double *)scratch, ticket, out);
     LAUNCHED();
     CU(cudaFreeAsync(scratch, st));
@@ -575,7 +651,7 @@ int csr_abs_sum(const void *z, int64_t n, double *out, void *stream) {
     CU(cudaMallocAsync(&scratch, (size_t)blocks * sizeof(double) + 16, st));
     unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * sizeof(double));
     CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
-    k_abs_sum<<<blocks, TPB, 0, st>>>((const float2 *)z, n, (double *)scratch, ticket, out);
+    launch(k_abs_sum, blocks, TPB, 0, st, (const float2 *)z, n, (double *)scratch, ticket, out);
     LAUNCHED();
     CU(cudaFreeAsync(scratch, st));
     return CSR_OK;
@@ -584,7 +660,7 @@ int csr_abs_sum(const void *z, int64_t n, double *out, void *stream) {
 int csr_axpy(double are, double aim, const void *x, const void *y, int64_t n,
              void *out, void *stream) {
     if (n <= 0) return CSR_OK;
-    k_axpy<<<ew_blocks(n), TPB, 0, (cudaStream_t)stream>>>(
+    launch(k_axpy, ew_blocks(n), TPB, 0, (cudaStream_t)stream, 
         make_float2((float)are, (float)aim), (const float2 *)x, (const float2 *)y, n,
         (float2 *)out);
     LAUNCHED();
@@ -690,7 +766,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     }
     const bool timed = p->iter_ms != nullptr;
     if (timed && p->tc.probe)
-        CU(cudaMemsetAsync(p->tc.probe, 0, 8 * sizeof(unsigned long long), st));
+        CU(cudaMemsetAsync(p->tc.probe, 0, PROBE_SLOTS * 4 * sizeof(unsigned long long), st));
     if (timed) {
         while ((int)p->iter_ev.size() < 2 * prm->admm_max_iters) {
             cudaEvent_t e;
@@ -701,7 +777,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     for (int it = 0; it < prm->admm_max_iters; ++it) {
         if (timed && p->flush_buf) {
             int64_t n16 = p->flush_bytes / 16;
-            k_flush<<<148 * 8, 512, 0, st>>>((uint4 *)p->flush_buf, n16, (unsigned)it);
+            launch(k_flush, 148 * 8, 512, 0, st, (uint4 *)p->flush_buf, n16, (unsigned)it);
             LAUNCHED();
         }
         if (timed) CU(cudaEventRecord(p->iter_ev[2 * it], st));
@@ -714,7 +790,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         if (timed) CU(cudaEventRecord(p->iter_ev[2 * it + 1], st));
     }
     CU(cudaEventRecord(p->ev[2], st));
-    k_copy_cur<<<ew_blocks(n), TPB, 0, st>>>(n, p->sc, p->rho[0], p->rho[1], (float2 *)rho_out);
+    launch(k_copy_cur, ew_blocks(n), TPB, 0, st, n, p->sc, p->rho[0], p->rho[1], (float2 *)rho_out);
     LAUNCHED();
     CU(cudaEventRecord(p->ev[3], st));
     CU(cudaStreamWaitEvent(caller, p->ev[3], 0));
@@ -768,6 +844,19 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
 int csr_debug_trace(csr_plan *p, unsigned long long *host, int64_t n) {
     if (!p || !p->tc.trace) return fail(CSR_ERR_ARG, "no trace buffer (set CSR_TRACE)");
     CU(cudaMemcpy(host, p->tc.trace, std::min<int64_t>(n, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
+    return CSR_OK;
+}
+
+int csr_plan_probe(csr_plan *p, int32_t slot, double *ms, int64_t *n) {
+    if (!p || !ms || !n) return fail(CSR_ERR_ARG, "null argument");
+    if (slot < 0 || slot >= PROBE_SLOTS) return fail(CSR_ERR_ARG, "probe slot out of range");
+    unsigned long long h[4] = {};
+    if (p->tc.probe) {
+        CU(cudaStreamSynchronize(p->stream));
+        CU(cudaMemcpy(h, p->tc.probe + 4 * slot, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    *n = (int64_t)h[3];
+    *ms = h[3] ? 1e-6 * (double)h[2] / (double)h[3] : 0.0;
     return CSR_OK;
 }
 

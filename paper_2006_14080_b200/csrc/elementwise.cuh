@@ -35,6 +35,7 @@ __host__ __device__ inline Geom make_geom(int T, int nx, int ny) {
 __global__ void k_factors(const double *__restrict__ coords, int64_t rows,
                           int nx, int ny, float2 *__restrict__ P0,
                           float2 *__restrict__ P1) {
+    pdl_enter();
     const double m2pi = -2.0 * 3.141592653589793;
     int64_t total = rows * (int64_t)(nx + ny);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -123,6 +124,7 @@ __device__ __forceinline__ void unflat(const Geom &g, int64_t p, int &t, int &x,
 
 __global__ void k_theta(Geom g, const float2 *__restrict__ img,
                         float2 *__restrict__ out) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
          i += (int64_t)gridDim.x * blockDim.x) {
         int comp = (int)(i / g.n);
@@ -134,6 +136,7 @@ __global__ void k_theta(Geom g, const float2 *__restrict__ img,
 
 __global__ void k_theta_adj(Geom g, const float2 *__restrict__ stack,
                             float2 *__restrict__ out) {
+    pdl_enter();
     StackRef u{stack, g};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -155,6 +158,7 @@ __device__ __forceinline__ float2 soft1(float2 z, float t) {
 
 __global__ void k_soft(const float2 *__restrict__ z, int64_t n, float t,
                        float2 *__restrict__ out) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = soft1(z[i], t);
@@ -164,6 +168,7 @@ __global__ void k_soft(const float2 *__restrict__ z, int64_t n, float t,
 __global__ void k_hdot(const float2 *__restrict__ a, const float2 *__restrict__ b,
                        int64_t n, double *partials, unsigned *ticket,
                        double *out) {
+    pdl_enter();
     double v[2] = {0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -180,6 +185,7 @@ __global__ void k_hdot(const float2 *__restrict__ a, const float2 *__restrict__ 
 
 __global__ void k_abs_sum(const float2 *__restrict__ z, int64_t n,
                           double *partials, unsigned *ticket, double *out) {
+    pdl_enter();
     double v[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -192,6 +198,7 @@ __global__ void k_abs_sum(const float2 *__restrict__ z, int64_t n,
 
 __global__ void k_axpy(float2 alpha, const float2 *__restrict__ x,
                        const float2 *y, int64_t n, float2 *out) {
+    pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = cadd(y[i], cmul(alpha, x[i]));
@@ -206,7 +213,18 @@ __device__ __forceinline__ float2 coil_combine(const float2 *__restrict__ ws,
                                                int t, int64_t pix) {
     float2 acc = make_float2(0.f, 0.f);
     if (!sens) {  // tensor-core partials: coils already combined
-        for (int s = 0; s < S; ++s) acc = cadd(acc, ws[((int64_t)s * T + t) * nxy + pix]);
+        // blocks of 8 predicated loads in flight (latency-bound at small n);
+        // the summation order stays s = 0, 1, 2, ...
+        for (int s0 = 0; s0 < S; s0 += 8) {
+            float2 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                v[j] = s0 + j < S ? ws[((int64_t)(s0 + j) * T + t) * nxy + pix]
+                                  : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (s0 + j < S) acc = cadd(acc, v[j]);
+        }
         return acc;
     }
     for (int c = 0; c < C; ++c) {
@@ -221,6 +239,7 @@ __device__ __forceinline__ float2 coil_combine(const float2 *__restrict__ ws,
 __global__ void k_adj_reduce(Geom g, int S, int C, const float2 *__restrict__ ws,
                              const float2 *__restrict__ sens,
                              float2 *__restrict__ out, const int *gate) {
+    pdl_enter();
     if (gate && !*gate) return;
     int64_t nxy = (int64_t)g.nx * g.ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
@@ -234,6 +253,7 @@ __global__ void k_adj_reduce(Geom g, int S, int C, const float2 *__restrict__ ws
 __global__ void k_normal_finish(Geom g, const float2 *__restrict__ fhf,
                                 const float2 *__restrict__ x, float hb,
                                 float2 *__restrict__ out) {
+    pdl_enter();
     ThetaOf th{x, g};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -290,6 +310,7 @@ struct AdmmBufs {
     float *tcs;
     double *mpart;
     unsigned *mtick;
+    unsigned long long *probe;  // live timing slots (csr_plan_probe) or null
 };
 
 enum FinOp { FIN_RHS = 0, FIN_AD = 1, FIN_XR = 2, FIN_POST = 3 };
@@ -344,6 +365,7 @@ __device__ void fin_post(DevScalars *s, IterLog *log, double num, double den) {
 
 // scalar update after the allreduce of b.loc (multi-rank)
 __global__ void k_finalize(AdmmBufs b, int op) {
+    pdl_enter();
     DevScalars *s = b.s;
     if (op == FIN_RHS || op == FIN_POST) {
         if (!s->admm_active) return;
@@ -360,6 +382,7 @@ __global__ void k_finalize(AdmmBufs b, int op) {
 // into fixed send buffers for the halo exchange (the ping-pong pointer is
 // only known on the device)
 __global__ void k_stage_frames(AdmmBufs b, Geom g, int sel, float2 *first, float2 *last) {
+    pdl_enter();
     if (!b.s->admm_active) return;
     const float2 *v = b.rho[b.s->cur ^ sel];
     const int64_t nf = (int64_t)g.nx * g.ny;
@@ -372,7 +395,9 @@ __global__ void k_stage_frames(AdmmBufs b, Geom g, int sel, float2 *first, float
 
 // mu+ = S(theta(rho) + eta)  (solver.py:178)
 __global__ void k_admm_mu(Geom g, AdmmBufs b) {
+    pdl_enter();
     if (!b.s->admm_active) return;
+    probe_enter(b.probe ? b.probe + 4 * PROBE_MU : nullptr);
     const float2 *rho = b.rho[b.s->cur];
     const int64_t nf = (int64_t)g.nx * g.ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
@@ -387,6 +412,7 @@ __global__ void k_admm_mu(Geom g, AdmmBufs b) {
         if (g.halo && comp == 2 && t == 0) b.sfirst[(int64_t)x * g.ny + y] = csub(m, b.eta[i]);
     }
     (void)nf;
+    probe_exit(b.probe ? b.probe + 4 * PROBE_MU : nullptr);
 }
 
 struct MuMinusEta {
@@ -403,7 +429,9 @@ struct MuMinusEta {
 // rhs = fhd + (beta/2) Theta^H (mu - eta) (solver.py:142-146); zero-start
 // CG init x = 0, r = d = rhs, tau = ||r||^2 (solver.py:99-108)
 __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
+    pdl_enter();
     if (!b.s->admm_active) return;
+    probe_enter(b.probe ? b.probe + 4 * PROBE_RHS : nullptr);
     float2 *x = b.rho[b.s->cur ^ 1];
     MuMinusEta u{b.mu, b.eta, g, b.hnext};
     double v[1] = {0.0};
@@ -430,12 +458,14 @@ __global__ void k_admm_rhs(Geom g, AdmmBufs b) {
         float m;
         if (grid_max(dmax, b.mpart, b.mtick, m)) b.tcs[6] = m;
     }
+    probe_exit(b.probe ? b.probe + 4 * PROBE_RHS : nullptr);
 }
 
 // ad = F^H F d (+ coil combine of split-K partials when ws != nullptr)
 //      + (beta/2) Theta^H Theta d ; <d, ad> -> alpha = tau / <d, ad>
 __global__ void k_cg_ad(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
                         const float2 *__restrict__ sens, int S, int C) {
+    pdl_enter();
     if (!b.s->cg_active) return;
     ThetaOf th{b.d, g, b.hprev, b.hnext};
     int64_t nxy = (int64_t)g.nx * g.ny;
@@ -468,6 +498,7 @@ __global__ void k_cg_ad(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
 // the allreduce runs on b.fhf, then k_cg_ad with ws == nullptr)
 __global__ void k_cg_fhf(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
                          const float2 *__restrict__ sens, int S, int C) {
+    pdl_enter();
     if (!b.s->cg_active) return;
     int64_t nxy = (int64_t)g.nx * g.ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n;
@@ -479,6 +510,7 @@ __global__ void k_cg_fhf(Geom g, AdmmBufs b, const float2 *__restrict__ ws,
 
 // x += alpha d ; r -= alpha ad ; tau' = ||r||^2 (solver.py:115-122)
 __global__ void k_cg_xr(Geom g, AdmmBufs b) {
+    pdl_enter();
     DevScalars *s = b.s;
     if (!s->cg_active) return;
     float2 *x = b.rho[s->cur ^ 1];
@@ -501,6 +533,7 @@ __global__ void k_cg_xr(Geom g, AdmmBufs b) {
 
 // d = r + (tau'/tau) d ; max|d| for the next forward's operand scale
 __global__ void k_cg_d(Geom g, AdmmBufs b) {
+    pdl_enter();
     DevScalars *s = b.s;
     if (!s->cg_active) return;
     float be = (float)s->beta_cg;
@@ -522,8 +555,10 @@ __global__ void k_cg_d(Geom g, AdmmBufs b) {
 // rho||^2 / ||rho||^2 (solver.py:149-155,192); loop guard
 // should_continue (solver.py:158-160); iteration record (solver.py:318-323)
 __global__ void k_admm_post(Geom g, AdmmBufs b) {
+    pdl_enter();
     DevScalars *s = b.s;
     if (!s->admm_active) return;
+    probe_enter(b.probe ? b.probe + 4 * PROBE_POST : nullptr);
     const float2 *rho = b.rho[s->cur];
     const float2 *xn = b.rho[s->cur ^ 1];
     double v[2] = {0.0, 0.0};
@@ -551,11 +586,13 @@ __global__ void k_admm_post(Geom g, AdmmBufs b) {
             fin_post(s, b.log, tot[0], tot[1]);
         }
     }
+    probe_exit(b.probe ? b.probe + 4 * PROBE_POST : nullptr);
 }
 
 // snapshots[admm_iter] = rho[cur]; idempotent, so it needs no gate
 __global__ void k_snapshot(int64_t n, const DevScalars *s, const float2 *r0,
                            const float2 *r1) {
+    pdl_enter();
     float2 *dst = s->snap;
     if (!dst) return;
     dst += (int64_t)s->admm_iter * n;

@@ -19,6 +19,7 @@ __global__ __launch_bounds__(256) void k_forward_simt(
     const float2 *__restrict__ P0, const float2 *__restrict__ P1,
     const float2 *__restrict__ sens, const float2 *__restrict__ img,
     float2 *__restrict__ kd, int M, int nx, int ny, int C, const int *gate) {
+    pdl_enter();
     if (gate && !*gate) return;
     __shared__ __align__(16) float2 As[SK][SP];  // As[y][k] = P1[k,y]
     __shared__ __align__(16) float2 Bs[SK][SP];  // Bs[y][x] = s_c*img
@@ -93,6 +94,7 @@ __global__ __launch_bounds__(256) void k_adjoint_simt(
     const float2 *__restrict__ P0, const float2 *__restrict__ P1,
     const float2 *__restrict__ kd, float2 *__restrict__ ws, int M, int nx,
     int ny, int C, int T, int kchunk, const int *gate) {
+    pdl_enter();
     if (gate && !*gate) return;
     __shared__ __align__(16) float2 As[SK][SP];  // As[k][x] = conj(P0[k,x]) d[k,c]
     __shared__ __align__(16) float2 Bs[SK][SP];  // Bs[k][y] = conj(P1[k,y])

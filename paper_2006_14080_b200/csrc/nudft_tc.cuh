@@ -54,7 +54,7 @@ struct TcPlan {
     int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
     bool fwd_ts = false;  // A-stationary forward (2*nyp <= 256)
     unsigned long long *trace = nullptr;  // CSR_TRACE: per-CTA timestamps
-    unsigned long long *probe = nullptr;   // [2][4] live timing slots: forward, adjoint
+    unsigned long long *probe = nullptr;   // [PROBE_SLOTS][4] live timing slots
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags
     int G_ts = 1, ntpg_ts = 1, fts_smem = 0;
     int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0;
@@ -88,6 +88,7 @@ __device__ __forceinline__ __half hneg(__half a) {
 // setup kernels (plan build)
 __global__ void k_tc_build_fa(const float2 *__restrict__ P1, int T, int64_t M, int64_t Mk,
                               int ny, int Kf, __half *hi, __half *lo) {
+    pdl_enter();
     int64_t total = (int64_t)T * Mk * (Kf / 2);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -106,6 +107,7 @@ __global__ void k_tc_build_fa(const float2 *__restrict__ P1, int T, int64_t M, i
 
 __global__ void k_tc_build_ga(const float2 *__restrict__ P1, int T, int64_t M, int64_t Mk,
                               int ny, int nyA, __half *hi, __half *lo) {
+    pdl_enter();
     int64_t total = (int64_t)T * nyA * Mk;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -124,6 +126,7 @@ __global__ void k_tc_build_ga(const float2 *__restrict__ P1, int T, int64_t M, i
 
 __global__ void k_tc_build_p0(const float2 *__restrict__ P0, int T, int64_t M, int64_t Mk,
                               int nx, int nxp, float2 *out) {
+    pdl_enter();
     int64_t total = (int64_t)T * Mk * nxp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -138,6 +141,7 @@ __global__ void k_tc_build_p0(const float2 *__restrict__ P0, int T, int64_t M, i
 // scales[4] = max component magnitude of the coil maps
 __global__ void k_tc_sens_absmax(const float2 *__restrict__ s, int64_t n, double *partials,
                                  unsigned *ticket, float *scales) {
+    pdl_enter();
     float v = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -156,6 +160,7 @@ struct TcArgs {
 // sigma_x for the image operand X = s_c * img: bound = 2 max|s| max|img|
 __global__ void k_tc_absmax_img(const float2 *__restrict__ img, int64_t n, double *partials,
                                 unsigned *ticket, float *scales, const int *gate) {
+    pdl_enter();
     if (gate && !*gate) return;
     float v = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -168,8 +173,11 @@ __global__ void k_tc_absmax_img(const float2 *__restrict__ img, int64_t n, doubl
 // X' = split(sigma_x * s_c * img_t) laid out as doubled rows (x, c, part)
 __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
                             const float2 *__restrict__ sens, float *scales,
-                            __half *hi, __half *lo, const int *gate) {
+                            __half *hi, __half *lo, const int *gate,
+                            unsigned long long *probe) {
+    pdl_enter();
     if (gate && !*gate) return;
+    probe_enter(probe);
     // exact power-of-two scale: |s_c * img| <= 2 max|s| max|img| (component-wise)
     const float sg = pow2_scale(2.f * scales[4] * scales[6]);
     if (blockIdx.x == 0 && threadIdx.x == 0) scales[5] = 0.f;  // k-space max (atomicMax)
@@ -202,6 +210,7 @@ __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
         H[e1] = pack2(ih, rh);
         L[e1] = pack2(il, rl);
     }
+    probe_exit(probe);
 }
 
 struct FwdParams {
@@ -215,31 +224,6 @@ struct FwdParams {
     const int *gate;
 };
 
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Live kernel timing (bench.py's roofline) without perturbing the launch
-// stream: pr = {~first CTA start, CTA ticket, sum of durations (ns),
-// launches}.  Every CTA stamps its start; the last CTA to finish adds
-// (its end - first start) and re-arms the slot for the next launch.
-__device__ __forceinline__ void probe_enter(unsigned long long *pr) {
-    if (pr && threadIdx.x == 0) atomicMax(&pr[0], ~(unsigned long long)gtimer());
-}
-__device__ __forceinline__ void probe_exit(unsigned long long *pr) {
-    if (!pr || threadIdx.x != 0) return;
-    __threadfence();
-    const unsigned long long n = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
-    if (atomicAdd(&pr[1], 1ull) == n - 1) {
-        const unsigned long long t1 = gtimer();
-        const unsigned long long t0 = ~atomicExch(&pr[0], 0ull);
-        atomicAdd(&pr[2], t1 - t0);
-        atomicAdd(&pr[3], 1ull);
-        atomicExch(&pr[1], 0ull);
-    }
-}
 
 // (offset arithmetic on the __shared__ pointer itself keeps the compiler's
 // address-space inference: LDS, not generic LD, for the smem operands)
@@ -254,6 +238,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmA_lo,
                  const __grid_constant__ CUtensorMap tmB_hi,
                  const __grid_constant__ CUtensorMap tmB_lo, FwdParams P) {
+    pdl_enter();
     using namespace sm100;
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
@@ -442,6 +427,7 @@ template <int CP>
 __global__ void __launch_bounds__(FTS_THREADS, 1)
     k_tc_forward_ts(const __grid_constant__ CUtensorMap tmB_hi,
                     const __grid_constant__ CUtensorMap tmB_lo, FwdTsParams P) {
+    pdl_enter();
     using namespace sm100;
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
@@ -654,6 +640,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
 __global__ void k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, float2 *kdi,
                             float2 *user, double *partials, unsigned *ticket, float *scales,
                             const int *gate) {
+    pdl_enter();
     if (gate && !*gate) return;
     int64_t total = (int64_t)a.T * a.Mk * a.Cp;
     int64_t gstride = total;
@@ -679,6 +666,7 @@ __global__ void k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, flo
 // user (T*M, C) k-space -> internal padded layout + sigma_d
 __global__ void k_tc_load_kd(TcArgs a, const float2 *__restrict__ user, float2 *kdi,
                              double *partials, unsigned *ticket, float *scales) {
+    pdl_enter();
     int64_t total = (int64_t)a.T * a.Mk * a.Cp;
     float v = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -811,6 +799,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmB_lo,
                  const __grid_constant__ CUtensorMap tmP0,
                  const __grid_constant__ CUtensorMap tmKd, AdjParams P) {
+    pdl_enter();
     using namespace sm100;
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
@@ -1274,14 +1263,14 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.sens = sens;
     cudaMemsetAsync(tc.tick, 0, 64, st);
     const int blocks = 148 * 8;
-    k_tc_build_fa<<<blocks, 256, 0, st>>>(P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo);
-    k_tc_build_ga<<<blocks, 256, 0, st>>>(P1, T, M, tc.Mk, ny, tc.nyA, tc.ga_hi, tc.ga_lo);
-    k_tc_build_p0<<<blocks, 256, 0, st>>>(P0, T, M, tc.Mk, nx, tc.nxp, tc.p0p);
+    launch(k_tc_build_fa, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo);
+    launch(k_tc_build_ga, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.nyA, tc.ga_hi, tc.ga_lo);
+    launch(k_tc_build_p0, blocks, 256, 0, st, P0, T, M, tc.Mk, nx, tc.nxp, tc.p0p);
     // max|s| (component-wise) for the image-operand scale bound
     {
         int64_t n = (int64_t)C * nx * ny;
         int nb = reduce_blocks(n, 256);
-        k_tc_sens_absmax<<<nb, 256, 0, st>>>(sens, n, tc.red, tc.tick, tc.scales);
+        launch(k_tc_sens_absmax, nb, 256, 0, st, sens, n, tc.red, tc.tick, tc.scales);
     }
     if (cudaGetLastError() != cudaSuccess) return 3;
     bool ok = tmap_f16_2d(&tc.tm_fa_hi, tc.fa_hi, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
@@ -1301,9 +1290,9 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
         default: break;
     }
-    if (tc_alloc(allocs, &p, 8 * sizeof(unsigned long long), ws_bytes, st)) return 2;
+    if (tc_alloc(allocs, &p, PROBE_SLOTS * 4 * sizeof(unsigned long long), ws_bytes, st)) return 2;
     tc.probe = (unsigned long long *)p;
-    cudaMemsetAsync(tc.probe, 0, 8 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(tc.probe, 0, PROBE_SLOTS * 4 * sizeof(unsigned long long), st);
     tc.fexp = getenv("CSR_FEXP") ? atoi(getenv("CSR_FEXP")) : 0;
     tc.aexp = getenv("CSR_EXP") ? atoi(getenv("CSR_EXP")) : 0;
     if (getenv("CSR_TRACE")) {
@@ -1325,16 +1314,17 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
 // the forward writes the k-space buffer directly (atomic max into scales[5])
 // instead of going through partials + k_tc_sum_kd.
 inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t st,
-                      const int *gate, bool in_loop = false) {
+                      const int *gate, bool in_loop = false, bool x_ready = false) {
     TcArgs a = tc_args(tc);
     const int64_t n = (int64_t)tc.T * tc.nx * tc.ny;
     if (!in_loop)
-        k_tc_absmax_img<<<reduce_blocks(n, 256), 256, 0, st>>>(img, n, tc.red, tc.tick,
+        launch(k_tc_absmax_img, reduce_blocks(n, 256), 256, 0, st, img, n, tc.red, tc.tick,
                                                                tc.scales, gate);
-    {
+    if (!x_ready) {  // else the fused CG tail already wrote X (cg_tail.cuh)
         int64_t total = (int64_t)tc.T * tc.nxp * tc.Cp * tc.nyp;
         int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-        k_tc_prep_x<<<nb, 256, 0, st>>>(a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate);
+        launch(k_tc_prep_x, nb, 256, 0, st, a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate,
+               tc.probe ? tc.probe + 4 * PROBE_PREP : nullptr);
     }
     const int G = tc.fwd_ts ? tc.G_ts : tc.G;
     const bool direct = in_loop && !user && G == 1;
@@ -1356,9 +1346,9 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.probe = tc.probe;
         dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
         switch (tc.Cp) {
-            case 4: k_tc_forward_ts<4><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
-            case 8: k_tc_forward_ts<8><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
-            default: k_tc_forward_ts<16><<<grid, FTS_THREADS, tc.fts_smem, st>>>(tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            case 4: launch(k_tc_forward_ts<4>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            case 8: launch(k_tc_forward_ts<8>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            default: launch(k_tc_forward_ts<16>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
         }
     } else {
         FwdParams P;
@@ -1373,24 +1363,24 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.probe = tc.probe;
         dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
         switch (tc.Cp) {
-            case 4: k_tc_forward<4><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            case 8: k_tc_forward<8><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            default: k_tc_forward<16><<<grid, TC_FWD_THREADS, tc.fwd_smem, st>>>(tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            case 4: launch(k_tc_forward<4>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            case 8: launch(k_tc_forward<8>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            default: launch(k_tc_forward<16>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
         }
     }
     if (!direct) {
         int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-        k_tc_sum_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, G, tc.kdp, tc.kdi, user,
+        launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, G, tc.kdp, tc.kdi, user,
                                                                tc.red, tc.tick, tc.scales, gate);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 // launches tc_forward makes (for the kernel-count bookkeeping)
-inline int tc_forward_launches(const TcPlan &tc, bool in_loop, bool user) {
+inline int tc_forward_launches(const TcPlan &tc, bool in_loop, bool user, bool x_ready = false) {
     const int G = tc.fwd_ts ? tc.G_ts : tc.G;
     const bool direct = in_loop && !user && G == 1;
-    return (in_loop ? 0 : 1) + 2 + (direct ? 0 : 1);
+    return (in_loop ? 0 : 1) + (x_ready ? 1 : 2) + (direct ? 0 : 1);
 }
 
 // kd already in tc.kdi (with sigma_d) when user == nullptr; else load it
@@ -1399,7 +1389,7 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     TcArgs a = tc_args(tc);
     if (user) {
         int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-        k_tc_load_kd<<<reduce_blocks(total, 256), 256, 0, st>>>(a, user, tc.kdi, tc.red, tc.tick,
+        launch(k_tc_load_kd, reduce_blocks(total, 256), 256, 0, st, a, user, tc.kdi, tc.red, tc.tick,
                                                                 tc.scales);
     }
     AdjParams P;
@@ -1409,7 +1399,7 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     P.chain = TC_MAX_CHAIN;
     P.exp_flags = tc.aexp;
     P.trace = tc.trace;
-    P.probe = tc.probe ? tc.probe + 4 : nullptr;
+    P.probe = tc.probe ? tc.probe + 4 * PROBE_ADJ : nullptr;
     P.kb_total = tc.kb_total;
     P.raw_bytes = tc.raw_bytes;
     P.n_raw = tc.adj_nraw;
@@ -1423,6 +1413,11 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     cfg.blockDim = dim3(ADJ_THREADS);
     cfg.dynamicSmemBytes = tc.adj_smem;
     cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaError_t e;
     switch (tc.Cp) {
         case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
