@@ -56,7 +56,8 @@ struct TcPlan {
     unsigned long long *trace = nullptr;  // CSR_TRACE: per-CTA timestamps
     unsigned long long *probe = nullptr;   // [PROBE_SLOTS][4] live timing slots
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags
-    int G_ts = 1, ntpg_ts = 1, fts_smem = 0;
+    int fts_ctas = 1, fts_smem = 0, fts_pieces = 1;
+    unsigned *ftick = nullptr;             // forward piece tickets [T * mt_f]
     int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
@@ -86,22 +87,29 @@ __device__ __forceinline__ __half hneg(__half a) {
 
 // ---------------------------------------------------------------------------
 // setup kernels (plan build)
+// lane_major (A-stationary forward): [row / 128][Kf / 8][row % 128][4 pairs],
+// so that the 32 lanes of a warp (32 consecutive rows) read one 16-byte chunk
+// each from 512 contiguous bytes when they load their rows into TMEM
 __global__ void k_tc_build_fa(const float2 *__restrict__ P1, int T, int64_t M, int64_t Mk,
-                              int ny, int Kf, __half *hi, __half *lo) {
+                              int ny, int Kf, __half *hi, __half *lo, int lane_major) {
     pdl_enter();
-    int64_t total = (int64_t)T * Mk * (Kf / 2);
+    const int hk = Kf / 2;
+    int64_t total = (int64_t)T * Mk * hk;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int y = (int)(i % (Kf / 2));
-        int64_t r = i / (Kf / 2);
+        int y = (int)(i % hk);
+        int64_t r = i / hk;
         int64_t k = r % Mk;
         int t = (int)(r / Mk);
         float2 v = (k < M && y < ny) ? P1[((int64_t)t * M + k) * ny + y] : make_float2(0.f, 0.f);
         __half h0, l0, h1, l1;
         split16(v.x, h0, l0);
         split16(v.y, h1, l1);
-        reinterpret_cast<uint32_t *>(hi)[i] = pack2(h0, h1);
-        reinterpret_cast<uint32_t *>(lo)[i] = pack2(l0, l1);
+        const int64_t o = lane_major
+                              ? (((r >> 7) * (hk / 4) + (y >> 2)) * 128 + (r & 127)) * 4 + (y & 3)
+                              : i;
+        reinterpret_cast<uint32_t *>(hi)[o] = pack2(h0, h1);
+        reinterpret_cast<uint32_t *>(lo)[o] = pack2(l0, l1);
     }
 }
 
@@ -397,12 +405,18 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     }
 }
 
-// Forward, A-stationary form (2*nyp <= 256).  Each CTA owns 128 samples of
-// one frame: their P1 rows (A, fp16 hi/lo) are loaded once into TMEM and
-// stay there while the image operand X' (B, 128 doubled rows = 64 complex
-// (x, c) columns per tile) streams through a 6-deep TMA ring; MMAs read A
-// from TMEM and only B from shared memory.  Double-buffered accumulators
-// (N = 128) let the row-dot epilogue of tile j overlap the MMAs of tile j+1.
+// Forward, A-stationary form (2*nyp <= 256), persistent.  The work is the
+// list of (sample tile m, N tile n) units, m-major; CTA b of the grid (one
+// per SM) takes the contiguous range [b*U/G, (b+1)*U/G), i.e. one or more
+// segments of N tiles of consecutive sample tiles.  Per segment the 128
+// samples' P1 rows (A, fp16 hi/lo) are loaded into TMEM once (from the
+// lane-major copy of the factor: fully coalesced) while the image operand
+// X' (B, 128 doubled rows = 64 complex (x, c) columns per tile) streams
+// through a TMA ring; MMAs read A from TMEM and only B from shared memory.
+// Double-buffered accumulators (N = 128) let the row-dot epilogue of tile j
+// overlap the MMAs of tile j+1.  A sample tile split across CTAs leaves one
+// partial per piece; the last piece to finish (ticket) sums them in piece
+// order, so the result does not depend on timing.
 //   TMEM: [0,128) A_hi, [128,256) A_lo, [256,384) / [384,512) accumulators.
 constexpr int FTS_STAGES = 3;
 constexpr int FTS_KPS = 2;             // K blocks per pipeline stage
@@ -412,31 +426,42 @@ constexpr int FTS_THREADS = 192;       // TMA, MMA, 4 epilogue (+A loader) warps
 struct FwdTsParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
     TcArgs a;
-    int mt_per_frame, nt_per_group;
-    int amax;
-    const uint32_t *fa_hi, *fa_lo;  // [T*Mk][Kf/2] packed fp16 pairs
+    int mt_per_frame;
+    int nt_tiles;    // N tiles per sample tile (Nf / 128)
+    int64_t units;   // T * mt_per_frame * nt_tiles
+    const uint4 *fa_hi, *fa_lo;  // lane-major: [mtile][Kf/8][128 rows] x 16 B
     const float2 *p0p;
-    float2 *kdp;  // [G][T][Mk][Cp]
-    const float *scales;
+    float2 *kdi;     // [T][Mk][Cp] (scaled result)
+    float2 *kdp;     // [pieces][T][Mk][Cp] partials of split tiles
+    unsigned *tick;  // [T * mt_per_frame][4] piece-ready flags (re-armed by piece 0)
+    float *scales;
     const int *gate;
     int exp_flags;  // profiling: 1 no MMA, 2 no TMA, 4 no epilogue math
     unsigned long long *trace;  // optional [grid][32] globaltimer stamps
 };
 
+// unit range of CTA b and the CTA that owns unit u
+__device__ __forceinline__ int64_t fts_u0(int64_t U, int G, int b) { return U * b / G; }
+__device__ __forceinline__ int fts_owner(int64_t U, int G, int64_t u) {
+    // largest b with U*b/G <= u
+    int b = (int)((u * G) / U);
+    while (b + 1 < G && fts_u0(U, G, b + 1) <= u) ++b;
+    while (b > 0 && fts_u0(U, G, b) > u) --b;
+    return b;
+}
+
 template <int CP>
 __global__ void __launch_bounds__(FTS_THREADS, 1)
     k_tc_forward_ts(const __grid_constant__ CUtensorMap tmB_hi,
                     const __grid_constant__ CUtensorMap tmB_lo, FwdTsParams P) {
-    pdl_enter();
     using namespace sm100;
-    if (P.gate && !*P.gate) return;
-    probe_enter(P.probe);
+    // Prologue overlapped with the previous kernel (programmatic launch):
+    // barrier init, TMEM allocation and the first segment's A rows read only
+    // static data; everything else waits in pdl_wait().
+    pdl_trigger();
     constexpr int XS = 64 / CP;  // x values per 128-row B tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    // A stage carries kps K blocks ([hi | lo] per block): each barrier wait of
-    // the MMA thread (~200+ cycles even when already satisfied) then covers
-    // kps x 768 MMA cycles
     constexpr int STAGE = FTS_KPS * 2 * FTS_B_TILE;
     const int kps = (P.a.Kf / 64) % FTS_KPS == 0 ? FTS_KPS : 1;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + FTS_STAGES * STAGE);
@@ -444,15 +469,16 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     uint64_t *tfull = empty + FTS_STAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *a_ready = tempty + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_ready + 1);
+    uint64_t *a_free = a_ready + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_free + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mtile = blockIdx.x;
-    const int t = mtile / P.mt_per_frame;
-    const int nt0 = blockIdx.y * P.nt_per_group, nt1 = nt0 + P.nt_per_group;
+    const int G = gridDim.x;
+    const int64_t U = P.units;
+    const int NT = P.nt_tiles;
+    const int64_t u0 = fts_u0(U, G, blockIdx.x), u1 = fts_u0(U, G, blockIdx.x + 1);
     const int nkb = P.a.Kf / 64;
-    unsigned long long *tr =
-        P.trace ? P.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 32 : nullptr;
+    unsigned long long *tr = P.trace ? P.trace + (size_t)blockIdx.x * 32 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (warp == 0 && lane == 0) {
@@ -467,6 +493,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             mbar_init(&tempty[i], 4);
         }
         mbar_init(a_ready, 4);
+        mbar_init(a_free, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -476,10 +503,58 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
-    if (warp == 0) {
+    // A rows of sample tile m -> TMEM (epilogue warps; lane = sample row).
+    // Lane-major factor copy: every load of a warp is 512 contiguous bytes;
+    // 16 chunks (hi + lo) in flight per thread per round.
+    const int nchunk = P.a.Kf / 8;  // 16-byte column chunks per row (hi or lo)
+    auto load_a = [&](int64_t m, uint32_t lane_base, int row) {
+        const uint4 *gh = P.fa_hi + (size_t)m * nchunk * 128 + row;
+        const uint4 *gl = P.fa_lo + (size_t)m * nchunk * 128 + row;
+        for (int c0 = 0; c0 < nchunk; c0 += 16) {
+            uint4 h[16], l[16];
+#pragma unroll
+            for (int v = 0; v < 16; ++v) {
+                h[v] = c0 + v < nchunk ? __ldg(gh + (size_t)(c0 + v) * 128) : make_uint4(0, 0, 0, 0);
+                l[v] = c0 + v < nchunk ? __ldg(gl + (size_t)(c0 + v) * 128) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                if (c0 + 8 * half >= nchunk) break;
+                uint32_t vh[32], vl[32];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const uint4 a = h[8 * half + v], b = l[8 * half + v];
+                    vh[4 * v] = a.x; vh[4 * v + 1] = a.y; vh[4 * v + 2] = a.z; vh[4 * v + 3] = a.w;
+                    vl[4 * v] = b.x; vl[4 * v + 1] = b.y; vl[4 * v + 2] = b.z; vl[4 * v + 3] = b.w;
+                }
+                tmem_st32(lane_base + (c0 + 8 * half) * 4, vh);
+                tmem_st32(lane_base + 128 + (c0 + 8 * half) * 4, vl);
+            }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(a_ready);
+    };
+    if (warp >= 2 && u0 < u1) {
+        const int q = warp & 3;
+        load_a(u0 / NT, tmem + ((uint32_t)(q * 32) << 16), q * 32 + lane);
+        if (tr && threadIdx.x == 64) tr[5] = gtimer();
+    }
+
+    pdl_wait();
+    const bool run = !P.gate || *P.gate;
+    if (run) probe_enter(P.probe);
+
+    if (!run) {
+    } else if (warp == 0) {
+        // ---- TMA producer over the CTA's units
         if (lane == 0) {
             int it = 0;
-            for (int nt = nt0; nt < nt1; ++nt) {
+            for (int64_t u = u0; u < u1; ++u) {
+                const int64_t m = u / NT;
+                const int nt = (int)(u - m * NT);
+                const int t = (int)(m / P.mt_per_frame);
                 const int brow = t * P.a.Nf + nt * 128;
                 for (int kb = 0; kb < nkb; kb += kps, ++it) {
                     const int s = it % FTS_STAGES;
@@ -488,24 +563,32 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     uint8_t *st = smem + s * STAGE;
                     mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : kps * 2 * FTS_B_TILE);
                     if (!(P.exp_flags & 2)) {
-                        for (int u = 0; u < kps; ++u) {
-                            uint8_t *sb = st + u * 2 * FTS_B_TILE;
-                            tma_load_2d(sb, &tmB_hi, &full[s], (kb + u) * 64, brow);
-                            tma_load_2d(sb + FTS_B_TILE, &tmB_lo, &full[s], (kb + u) * 64, brow);
+                        for (int v = 0; v < kps; ++v) {
+                            uint8_t *sb = st + v * 2 * FTS_B_TILE;
+                            tma_load_2d(sb, &tmB_hi, &full[s], (kb + v) * 64, brow);
+                            tma_load_2d(sb + FTS_B_TILE, &tmB_lo, &full[s], (kb + v) * 64, brow);
                         }
                     }
                 }
             }
         }
     } else if (warp == 1) {
+        // ---- MMA issuer
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, 128);
-            mbar_wait(a_ready, 0);
-            tc_fence_after();
-            if (tr) tr[2] = gtimer();
             const uint32_t a_hi = tmem, a_lo = tmem + 128;
-            int it = 0, tc = 0;
-            for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+            int it = 0, tc = 0, seg = 0;
+            int64_t m_prev = -1;
+            for (int64_t u = u0; u < u1; ++u, ++tc) {
+                const int64_t m = u / NT;
+                if (m != m_prev) {  // new segment: wait for its A
+                    if (m_prev >= 0) mma_commit(a_free);  // old A is free after these MMAs
+                    mbar_wait(a_ready, seg & 1);
+                    tc_fence_after();
+                    if (tr && seg < 2) tr[2 + seg * 4] = gtimer();
+                    ++seg;
+                    m_prev = m;
+                }
                 const int ab = tc & 1;
                 const uint32_t aph = (tc >> 1) & 1;
                 mbar_wait(&tempty[ab], aph ^ 1);
@@ -516,16 +599,15 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     const uint32_t ph = (it / FTS_STAGES) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    if (tr && it < 8) tr[8 + it] = gtimer();
-                    for (int u = 0; u < kps; ++u) {
-                        const uint32_t st = smem_u32(smem + s * STAGE + u * 2 * FTS_B_TILE);
+                    for (int v = 0; v < kps; ++v) {
+                        const uint32_t st = smem_u32(smem + s * STAGE + v * 2 * FTS_B_TILE);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            const uint32_t ac = (kb + u) * 32 + kk * 8;
+                            const uint32_t ac = (kb + v) * 32 + kk * 8;
                             const uint64_t dbh = desc_sw128(st + kk * 32);
                             const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
                             if (P.exp_flags & 1) continue;
-                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, ((kb + u) | kk) != 0);
+                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, ((kb + v) | kk) != 0);
                             mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
                             mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
                         }
@@ -533,64 +615,26 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[ab]);
-                if (tr && tc < 4) tr[16 + tc] = gtimer();
+                if (tr && tc < 8) tr[16 + tc] = gtimer();
             }
             if (tr) tr[3] = gtimer();
         }
-    } else {
-        // warps 2..5: TMEM lane quarter q; lane m = sample row of the tile
+    } else if (warp >= 2) {
+        // ---- epilogue warps 2..5: TMEM lane quarter q, lane = sample row
         const int q = warp & 3;
         const int row = q * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-        // ---- A: this sample's P1 row (hi, lo) -> TMEM, once
-        {
-            const int64_t grow = (int64_t)mtile * 128 + row;  // = t*Mk + local row
-            const int ncol = P.a.Kf / 2;
-            const uint4 *gh = reinterpret_cast<const uint4 *>(P.fa_hi + grow * ncol);
-            const uint4 *gl = reinterpret_cast<const uint4 *>(P.fa_lo + grow * ncol);
-            for (int c0 = 0; c0 < ncol; c0 += 32) {
-                uint32_t vh[32], vl[32];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint4 h = __ldg(gh + c0 / 4 + u), l = __ldg(gl + c0 / 4 + u);
-                    vh[4 * u] = h.x; vh[4 * u + 1] = h.y; vh[4 * u + 2] = h.z; vh[4 * u + 3] = h.w;
-                    vl[4 * u] = l.x; vl[4 * u + 1] = l.y; vl[4 * u + 2] = l.z; vl[4 * u + 3] = l.w;
-                }
-                tmem_st32(lane_base + c0, vh);
-                tmem_st32(lane_base + 128 + c0, vl);
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(a_ready);
-            if (tr && threadIdx.x == 64) tr[5] = gtimer();
-        }
-        // ---- per tile: kd[k, c] += sum_x P0[k, x] G[k, (x, c)]
-        const int64_t kloc = (int64_t)(mtile % P.mt_per_frame) * 128 + row;
-        const bool valid = kloc < P.a.M;
-        const float2 *p0row = P.p0p + ((int64_t)t * P.a.Mk + kloc) * P.a.nxp;
-        constexpr int U = CP > 16 ? CP / 16 : 1;
-        float2 acc[CP];
-#pragma unroll
-        for (int c = 0; c < CP; ++c) acc[c] = make_float2(0.f, 0.f);
-        int tc = 0;
-        for (int nt = nt0; nt < nt1; ++nt, ++tc) {
-            const int ab = tc & 1;
-            const uint32_t aph = (tc >> 1) & 1;
-            const int xbase = nt * XS;
-            // this tile's P0 values are loaded before waiting on the MMA
-            float2 p0v[XS];
-#pragma unroll
-            for (int i = 0; i < XS; ++i)
-                p0v[i] = valid ? p0row[xbase + i] : make_float2(0.f, 0.f);
-            mbar_wait(&tfull[ab], aph);
-            tc_fence_after();
+        const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
+        const int64_t Mk = P.a.Mk;
+        constexpr int UU = CP > 16 ? CP / 16 : 1;
+        // drain accumulator buffer ab (tile column block nt) into acc
+        auto drain = [&](int ab, const float2 (&p0v)[XS], float2 (&acc)[CP]) {
             const uint32_t taddr = lane_base + 256 + ab * 128;
 #pragma unroll
-            for (int chb = 0; chb < 4; chb += U) {
+            for (int chb = 0; chb < 4; chb += UU) {
                 if (P.exp_flags & 4) break;
 #pragma unroll
-                for (int h = 0; h < U; ++h) {
+                for (int h = 0; h < UU; ++h) {
                     uint32_t r[32];
                     tmem_ld32(taddr + (chb + h) * 32, r);
                     tmem_ld_wait();
@@ -606,29 +650,106 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[ab]);
-            if (tr && threadIdx.x == 64 && tc < 4) tr[24 + tc] = gtimer();
+        };
+        int tc = 0, seg = 0;
+        for (int64_t us = u0; us < u1; ++seg) {
+            const int64_t m = us / NT;
+            const int64_t ue = min(u1, (m + 1) * NT);
+            const int t = (int)(m / P.mt_per_frame);
+            const bool last_seg = ue == u1;
+            // ---- this segment's N tiles: kd[k, c] += sum_x P0[k, x] G[k, (x, c)]
+            const int64_t kloc = (int64_t)(m % P.mt_per_frame) * 128 + row;
+            const bool valid = kloc < P.a.M;
+            const float2 *p0row = P.p0p + ((int64_t)t * Mk + kloc) * P.a.nxp;
+            const int b_first = fts_owner(U, G, m * NT);
+            const int b_last = fts_owner(U, G, (m + 1) * NT - 1);
+            const int npieces = b_last - b_first + 1;
+            const int piece = blockIdx.x - b_first;
+            const int64_t grow = (int64_t)t * Mk + kloc;
+            float2 acc[CP];
+#pragma unroll
+            for (int c = 0; c < CP; ++c) acc[c] = make_float2(0.f, 0.f);
+            float2 p0v[XS];
+            for (int64_t u = us; u < ue; ++u, ++tc) {
+                const int nt = (int)(u - m * NT);
+                const int ab = tc & 1;
+                const uint32_t aph = (tc >> 1) & 1;
+#pragma unroll
+                for (int i = 0; i < XS; ++i)
+                    p0v[i] = valid ? p0row[nt * XS + i] : make_float2(0.f, 0.f);
+                if (u + 1 == ue && !last_seg) {
+                    // the segment's last tile: load the next segment's A as
+                    // soon as the MMAs release the old one (the tile's
+                    // accumulator stays put in its TMEM buffer meanwhile),
+                    // so the tensor core waits only for the A load
+                    mbar_wait(a_free, seg & 1);
+                    tc_fence_after();
+                    load_a(ue / NT, lane_base, row);
+                    if (tr && threadIdx.x == 64 && seg < 1) tr[9] = gtimer();
+                }
+                if (u + 1 == ue && piece == 0 && npieces > 1) {
+                    // the other pieces of this tile finished long ago (their
+                    // CTAs started on it): fold them in before the last drain
+                    for (int pc = 1; pc < npieces; ++pc) {
+                        unsigned f = 0;
+                        const unsigned *flag = P.tick + m * 4 + pc;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
+                                         : "=r"(f) : "l"(flag) : "memory");
+                        } while (f == 0u);
+                    }
+                }
+                mbar_wait(&tfull[ab], aph);
+                tc_fence_after();
+                drain(ab, p0v, acc);
+                if (tr && threadIdx.x == 64 && tc < 8) tr[24 + tc] = gtimer();
+            }
+            // ---- finish the segment.  A sample tile split across CTAs: the
+            // CTA holding its first units (piece 0; the tile is that CTA's
+            // last segment, so it is the last to get there) sums pieces
+            // 0, 1, ... in that order once their flags are up.
+            if (piece > 0) {
+                float2 *mine = P.kdp + ((int64_t)(piece - 1) * P.a.T * Mk + grow) * CP;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) mine[c] = acc[c];
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (threadIdx.x == 64) {
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.tick + m * 4 + piece),
+                                 "r"(1u)
+                                 : "memory");
+                }
+            } else {
+                for (int pc = 1; pc < npieces; ++pc) {
+                    const float2 *src = P.kdp + ((int64_t)(pc - 1) * P.a.T * Mk + grow) * CP;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) acc[c] = cadd(acc[c], __ldcg(src + c));
+                }
+                if (npieces > 1) {
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (threadIdx.x < 64 + npieces - 1 && threadIdx.x >= 64)
+                        P.tick[m * 4 + 1 + (threadIdx.x - 64)] = 0u;  // re-arm
+                }
+                // max|kd| for the adjoint's operand scale (order-free)
+                float mx = 0.f;
+#pragma unroll
+                for (int c = 0; c < CP; ++c)
+                    mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(P.scales + 5), __float_as_uint(mx));
+                if (valid) {
+                    float2 *out = P.kdi + grow * CP;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
+                }
+            }
+            us = ue;
         }
         if (tr && threadIdx.x == 64) tr[4] = gtimer();
-        if (P.amax) {  // max|kd| for the adjoint's operand scale (order-free)
-            float mx = 0.f;
-            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
-#pragma unroll
-            for (int c = 0; c < CP; ++c)
-                mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(const_cast<float *>(P.scales) + 5),
-                                     __float_as_uint(mx));
-        }
-        if (valid) {
-            const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
-            float2 *out = P.kdp + (((int64_t)blockIdx.y * P.a.T + t) * P.a.Mk + kloc) * CP;
-#pragma unroll
-            for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
-        }
     }
     __syncthreads();
-    probe_exit(P.probe);
+    if (run) probe_exit(P.probe);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -1182,20 +1303,29 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup)
     tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS");
     if (tc.fwd_ts) {
-        const int nt128 = tc.Nf / 128, nkb = tc.Kf / 64;
-        int64_t best = INT64_MAX;
-        for (int g = 1; g <= nt128; ++g) {
-            if (nt128 % g) continue;
-            const int64_t waves = (mtiles * g + 147) / 148;
-            const int64_t cost = waves * ((int64_t)(nt128 / g) * nkb * 768 + 6000);
-            if (cost < best) {
-                best = cost;
-                tc.G_ts = g;
-            }
-        }
-        tc.ntpg_ts = nt128 / tc.G_ts;
+        const int NTt = tc.Nf / 128;
+        const int64_t units = mtiles * NTt;
         tc.fts_smem = FTS_STAGES * FTS_KPS * 2 * FTS_B_TILE + 1024 + 256;
-        G = std::max(G, tc.G_ts);
+        // CTAs = SMs (persistent); pieces of a sample tile split across CTAs
+        // are limited to the 4 flag slots per tile
+        auto max_pieces = [&](int64_t Gc) {
+            auto owner = [&](int64_t u) {
+                int64_t b = u * Gc / units;
+                while (b + 1 < Gc && units * (b + 1) / Gc <= u) ++b;
+                while (b > 0 && units * b / Gc > u) --b;
+                return b;
+            };
+            int mp = 1;
+            for (int64_t m = 0; m < mtiles; ++m)
+                mp = std::max<int>(mp, (int)(owner((m + 1) * NTt - 1) - owner(m * NTt) + 1));
+            return mp;
+        };
+        int64_t Gc = std::min<int64_t>(148, units);
+        int maxp = max_pieces(Gc);
+        while (maxp > 4 && Gc > mtiles) maxp = max_pieces(--Gc);
+        tc.fts_ctas = (int)Gc;
+        G = std::max(G, maxp - 1);  // kdp holds pieces 1.. (piece 0 stays in registers)
+        tc.fts_pieces = maxp;
     }
     // adjoint split-K
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
@@ -1259,11 +1389,14 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     TCA(tc.scales, 64, ws_bytes);
     TCA(tc.red, 4 * 148 * 8, ws_bytes);
     TCA(tc.tick, 64, ws_bytes);
+    TCA(tc.ftick, (size_t)T * tc.mt_f * 16 + 16, ws_bytes);  // 4 piece flags per tile
+    cudaMemsetAsync(tc.ftick, 0, (size_t)T * tc.mt_f * 16 + 16, st);
 #undef TCA
     tc.sens = sens;
     cudaMemsetAsync(tc.tick, 0, 64, st);
     const int blocks = 148 * 8;
-    launch(k_tc_build_fa, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo);
+    launch(k_tc_build_fa, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo,
+           tc.fwd_ts ? 1 : 0);
     launch(k_tc_build_ga, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.nyA, tc.ga_hi, tc.ga_lo);
     launch(k_tc_build_p0, blocks, 256, 0, st, P0, T, M, tc.Mk, nx, tc.nxp, tc.p0p);
     // max|s| (component-wise) for the image-operand scale bound
@@ -1326,31 +1459,42 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         launch(k_tc_prep_x, nb, 256, 0, st, a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate,
                tc.probe ? tc.probe + 4 * PROBE_PREP : nullptr);
     }
-    const int G = tc.fwd_ts ? tc.G_ts : tc.G;
-    const bool direct = in_loop && !user && G == 1;
-    float2 *kdp = direct ? tc.kdi : tc.kdp;
     if (tc.fwd_ts) {
+        // persistent A-stationary forward: always writes the scaled k-space
+        // into kdi (and max|kd| into scales[5])
         FwdTsParams P;
         P.a = a;
         P.mt_per_frame = tc.mt_f;
-        P.nt_per_group = tc.ntpg_ts;
-        P.amax = direct ? 1 : 0;
-        P.fa_hi = reinterpret_cast<const uint32_t *>(tc.fa_hi);
-        P.fa_lo = reinterpret_cast<const uint32_t *>(tc.fa_lo);
+        P.nt_tiles = tc.Nf / 128;
+        P.units = (int64_t)tc.T * tc.mt_f * P.nt_tiles;
+        P.fa_hi = reinterpret_cast<const uint4 *>(tc.fa_hi);
+        P.fa_lo = reinterpret_cast<const uint4 *>(tc.fa_lo);
         P.p0p = tc.p0p;
-        P.kdp = kdp;
+        P.kdi = tc.kdi;
+        P.kdp = tc.kdp;
+        P.tick = tc.ftick;
         P.scales = tc.scales;
         P.gate = gate;
         P.exp_flags = tc.fexp;
         P.trace = tc.trace;
         P.probe = tc.probe;
-        dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
+        dim3 grid((unsigned)tc.fts_ctas);
         switch (tc.Cp) {
             case 4: launch(k_tc_forward_ts<4>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
             case 8: launch(k_tc_forward_ts<8>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
             default: launch(k_tc_forward_ts<16>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
         }
-    } else {
+        if (user) {  // (T*M, C) copy for the caller
+            int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
+            launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, 1, tc.kdi, tc.kdi, user,
+                   tc.red, tc.tick, tc.scales, gate);
+        }
+        return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    }
+    const int G = tc.G;
+    const bool direct = in_loop && !user && G == 1;
+    float2 *kdp = direct ? tc.kdi : tc.kdp;
+    {
         FwdParams P;
         P.a = a;
         P.mt_per_frame = tc.mt_f;
@@ -1378,8 +1522,8 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
 
 // launches tc_forward makes (for the kernel-count bookkeeping)
 inline int tc_forward_launches(const TcPlan &tc, bool in_loop, bool user, bool x_ready = false) {
-    const int G = tc.fwd_ts ? tc.G_ts : tc.G;
-    const bool direct = in_loop && !user && G == 1;
+    if (tc.fwd_ts) return (in_loop ? 0 : 1) + (x_ready ? 1 : 2) + (user ? 1 : 0);
+    const bool direct = in_loop && !user && tc.G == 1;
     return (in_loop ? 0 : 1) + (x_ready ? 1 : 2) + (direct ? 0 : 1);
 }
 

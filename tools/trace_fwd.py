@@ -23,9 +23,8 @@ ctas = tr[tr[:, 0] > 0]
 t0 = ctas[:, 0].min()
 rel = lambda c: (ctas[:, c] - t0) / 1e3
 print("CTAs", len(ctas))
-for name, c in [("entry", 0), ("setup", 1), ("A loaded (epi)", 5), ("mma a_ready", 2), ("mma done", 3), ("epi done", 4)]:
-    v = rel(c); print(f"{name:16s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")
+for name, c in [("entry", 0), ("setup", 1), ("A0 loaded (epi)", 5), ("mma a_ready 0", 2), ("A1 loaded (epi)", 9), ("mma a_ready 1", 6), ("mma done", 3), ("epi done", 4)]:
+    v = ctas[:, c]; v = (v[v > 0] - t0) / 1e3
+    if len(v): print(f"{name:16s} n {len(v):4d} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")
 for i in range(8):
-    v = rel(8 + i); print(f"stage {i} full    med {np.median(v):7.2f} us")
-for i in range(4):
     v = rel(16 + i); w = rel(24 + i); print(f"tile {i} mma-commit med {np.median(v):7.2f}  epi-done med {np.median(w):7.2f} us")
