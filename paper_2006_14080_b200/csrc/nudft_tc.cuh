@@ -920,10 +920,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmB_lo,
                  const __grid_constant__ CUtensorMap tmP0,
                  const __grid_constant__ CUtensorMap tmKd, AdjParams P) {
-    pdl_enter();
     using namespace sm100;
-    if (P.gate && !*P.gate) return;
-    probe_enter(P.probe);
+    // Prologue overlapped with the forward (programmatic launch): barrier
+    // init, TMEM allocation and the first B-ring stages (static factor) do
+    // not depend on it; every role waits in pdl_wait() before touching kd,
+    // the scales or the gate.
+    pdl_trigger();
     constexpr int XS = 64 / CP;  // x values per tile
     constexpr int IN_STAGE = adj_in_stage_bytes(CP);
     constexpr int OFF_D = 32 * XS * 8, OFF_DP = OFF_D + 32 * CP * 8;
@@ -982,12 +984,29 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the first B stages are free by construction: fetch them right away
+    const int pre = min(nkb, ADJ_STAGES);
+    const int brow = t * P.a.nyA + nt * 128;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < pre; ++i) {
+            uint8_t *st = smem + i * ADJ_B_STAGE;
+            mbar_arrive_expect_tx(&full[i], ADJ_B_STAGE);
+            tma_load_2d(st, &tmB_hi, &full[i], (kb0 + i) * 64, brow);
+            tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[i], (kb0 + i) * 64, brow);
+        }
+    }
+    pdl_wait();
+    const bool run = !P.gate || *P.gate;
+    if (run) probe_enter(P.probe);
 
-    if (warp == 0) {
+    if (!run) {
+        // gated off: let the prefetched stages land before the CTA exits
+        if (warp == 0 && lane == 0)
+            for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0);
+    } else if (warp == 0) {
         // ---- B ring producer: conj(P1)^T hi / lo tiles
         if (lane == 0) {
-            const int brow = t * P.a.nyA + nt * 128;
-            for (int i = 0; i < nkb; ++i) {
+            for (int i = pre; i < nkb; ++i) {
                 const int kb = kb0 + i;
                 const int s = i % ADJ_STAGES;
                 wait_slow(&empty[s], ((i / ADJ_STAGES) & 1) ^ 1);
@@ -1130,7 +1149,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         }
     }
     float sum[128];  // epilogue warps: running sums of row m over the 128 y
-    if (warp >= ADJ_W_EPI) {
+    if (run && warp >= ADJ_W_EPI) {
         // ---- epilogue: drain every chain into the register sums
         const int q = warp & 3;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
@@ -1157,7 +1176,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         }
     }
     __syncthreads();  // all MMAs and TMA loads are done: the B ring is free
-    if (warp >= ADJ_W_EPI) {
+    if (run && warp >= ADJ_W_EPI) {
         const int m = (warp & 3) * 32 + lane;
 #pragma unroll
         for (int y = 0; y < 128; ++y) sum_s[y * ADJ_SUM_LD + m] = sum[y];
@@ -1167,7 +1186,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     // warps: thread e handles pixel row y = e % 128 for the x values
     // xq = e / 128 (mod warps / 4) of the tile, reading the transposed sums
     // (padded rows: conflict-free) and the coil maps with y-coalesced loads
-    {
+    if (run) {
         const float inv = 1.f / pow2_scale(P.scales[5]);
         const int e = threadIdx.x & 127, grp = threadIdx.x >> 7;
         const int y = nt * 128 + e;
@@ -1195,7 +1214,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         }
     }
     __syncthreads();
-    probe_exit(P.probe);
+    if (run) probe_exit(P.probe);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
