@@ -37,22 +37,30 @@ struct CgTailArgs {
     unsigned long long *stamps; // debug: phase timestamps of block 0 (CSR_TRACE)
 };
 
-// Sense-reversing grid barrier; the kernel is launched cooperatively, so all
-// blocks are co-resident.
-__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+// Grid barrier for the cooperative launch (all blocks co-resident).  bar[1]
+// counts completed barriers; each block reads it once at kernel start
+// (gen0), so barrier k only has to wait for bar[1] == gen0 + k: one
+// release-add to arrive, one acquire spin to leave, no extra fences.
+__device__ __forceinline__ unsigned grid_gen(const unsigned *bar) {
+    unsigned g;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    return g;
+}
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0u;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(bar) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
         } else {
-            while (*gen == g0) __nanosleep(20);
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+            } while ((int)(g - target) < 0);
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -116,6 +124,8 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
     const int cg_iter = s->cg_iter + 1, cg_max = s->cg_max, cur = s->cur;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    __shared__ unsigned gen0;
+    if (threadIdx.x == 0) gen0 = grid_gen(A.bar);  // before anyone can arrive
 
     // ---- phase A: Ad and <d, Ad>
     {
@@ -135,7 +145,7 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
         block_partials<2>(v, A.part);
     }
     TAIL_STAMP(1);
-    grid_barrier(A.bar);
+    grid_barrier(A.bar, gen0 + 1);
     double dad[2];
     TAIL_STAMP(2);
     all_totals<2>(A.part, dad);
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
         }
     }
     TAIL_STAMP(4);
-    grid_barrier(A.bar);
+    grid_barrier(A.bar, gen0 + 2);
     double tn;
     TAIL_STAMP(5);
     float rmax_all;
