@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -132,17 +133,36 @@ int dalloc(csr_plan *p, T **ptr, size_t count, int64_t *acct) {
         if (rc_ != CSR_OK) return rc_; \
     } while (0)
 
+// CSR_HOST_TIMING=1: host-side phase times of plan build / solve on stderr
+struct HostTimer {
+    bool on = getenv("CSR_HOST_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char *what) {
+        if (!on) return;
+        auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[csr host] %-28s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - t0).count());
+    }
+};
+
 int check_device(int dev) {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0)
         return fail(CSR_ERR_CUDA, "no CUDA device available (csrecon_b200 has no CPU fallback)");
     if (dev < 0 || dev >= n) return fail(CSR_ERR_ARG, "device ordinal out of range");
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, dev));
-    if (prop.major != 10)
+    // cached per device: cudaGetDeviceProperties costs milliseconds
+    static int checked[64] = {};
+    if (dev < 64 && checked[dev]) return CSR_OK;
+    int major = 0;
+    CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) {
+        cudaDeviceProp prop;
+        CU(cudaGetDeviceProperties(&prop, dev));
         return fail(CSR_ERR_CUDA, std::string("csrecon_b200 is built for sm_100a; device is ") +
                                       prop.name);
+    }
+    if (dev < 64) checked[dev] = 1;
     return CSR_OK;
 }
 
@@ -426,8 +446,10 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         desc->n_samples < 1)
         return fail(CSR_ERR_SHAPE, "plan dimensions must all be >= 1");
     if (!desc->coords || !desc->sens) return fail(CSR_ERR_ARG, "coords and sens are required");
+    HostTimer ht;
     TRY(check_device(desc->device));
     CU(cudaSetDevice(desc->device));
+    ht.mark("check device");
     csr_plan *p = new csr_plan();
     p->dev = desc->device;
     p->T = desc->n_frames;
@@ -452,6 +474,7 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, "stream create failed"));
     p->stream = st;
+    ht.mark("stream");
     if ((rc = dalloc(p, &p->P0, (size_t)(rows * p->nx), &p->factor_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->P1, (size_t)(rows * p->ny), &p->factor_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->sens, (size_t)(p->C * nxy), &p->factor_bytes))) return cleanup(rc);
@@ -474,11 +497,13 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         g_launches.fetch_add(1);
         if (cudaGetLastError() != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "k_factors launch"));
     }
+    ht.mark("factors enqueued");
     // tensor-core operand build (returns tc.enabled=false for shapes it
     // does not tile; the SIMT kernels then handle the plan)
     if ((rc = tc_plan_build(p->tc, p->T, p->nx, p->ny, p->C, p->M, p->P0, p->P1, p->sens, st,
                             &p->factor_bytes, &p->ws_bytes, p->allocs)))
         return cleanup(fail(rc, "tensor-core plan: " + g_err));
+    ht.mark("tc plan");
     // workspace
     if ((rc = dalloc(p, &p->kd, (size_t)(rows * p->C), &p->ws_bytes))) return cleanup(rc);
     if (p->tc.enabled) {
@@ -523,9 +548,11 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     if ((rc = dalloc(p, &p->sc, 1, &p->ws_bytes))) return cleanup(rc);
     if (cudaMemsetAsync(p->tickets, 0, 16 * sizeof(unsigned), st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, "memset"));
+    ht.mark("workspace");
     if (cudaStreamSynchronize(st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, std::string("plan build: ") +
                                               cudaGetErrorString(cudaGetLastError())));
+    ht.mark("plan synced");
     *out = p;
     return CSR_OK;
 }
@@ -686,6 +713,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         return fail(CSR_ERR_ARG, "admm_rtol and cg_atol must be > 0");
     if (prm->admm_max_iters < 1 || prm->cg_max_iters < 1)
         return fail(CSR_ERR_ARG, "iteration caps must be >= 1");
+    HostTimer ht;
     CU(cudaSetDevice(p->dev));
     cudaStream_t caller = (cudaStream_t)stream;
     cudaStream_t st = p->stream;
@@ -728,6 +756,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
                            cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(p->sc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
     CU(cudaEventRecord(p->ev[1], st));
+    ht.mark("setup enqueued");
     // ---- ADMM loop as a CUDA graph of one iteration
     AdmmBufs b = admm_bufs(p, prm);
     std::vector<double> key = {prm->lam, prm->lam_t, prm->beta,
@@ -764,6 +793,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         p->kernels_per_iter = nk;
         p->graph_key = key;
     }
+    ht.mark("graph ready");
     const bool timed = p->iter_ms != nullptr;
     if (timed && p->tc.probe)
         CU(cudaMemsetAsync(p->tc.probe, 0, PROBE_SLOTS * 4 * sizeof(unsigned long long), st));
@@ -800,7 +830,9 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     CU(cudaMemcpyAsync(&hs, p->sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(hl.data(), p->log, sizeof(IterLog) * prm->admm_max_iters,
                        cudaMemcpyDeviceToHost, st));
+    ht.mark("loop enqueued");
     CU(cudaStreamSynchronize(st));
+    ht.mark("solve synced");
     for (int i = 0; i < hs.admm_iter; ++i) {
         log[i].iteration = hl[i].iteration;
         log[i].cg_iterations = hl[i].cg_iterations;
