@@ -36,8 +36,9 @@ PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 METRIC = "ADMM iters/s"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-# kernel, from one `ncu --set full` capture (profiles/r01_ncu_adjoint_c*.txt)
-TRAFFIC = {}
+# kernel (config 1: the forward GEMM), from one `ncu --set full` capture
+# (profiles/r01_ncu_full.txt; cold cache: the factors come from HBM)
+TRAFFIC = {1: 35704576 + 256}
 
 
 def peaks():
