@@ -181,6 +181,15 @@ int csr_plan_kernel_times(csr_plan *plan, double *fwd_ms, double *adj_ms,
  * tail, 6 ADMM post-update. */
 int csr_plan_probe(csr_plan *plan, int32_t slot, double *ms, int64_t *n);
 
+/* simulate_kspace (acquisition.py:233-257), double precision on the GPU:
+ * kspace[t*M + k, c] = sum_{x,y} sens[c,x,y] image[t,x,y]
+ *                      exp(-2 pi i (kx_k (x - nx/2) + ky_k (y - ny/2))).
+ * coords (T*M, 2) f64, sens (C, nx, ny) c128, image (T, nx, ny) c128,
+ * kspace (T*M, C) c128: all DEVICE pointers; stream-ordered. */
+int csr_simulate_kspace(int32_t nx, int32_t ny, int32_t n_frames, int32_t n_coils,
+                        int64_t n_samples, const double *coords, const void *sens,
+                        const void *image, void *kspace, void *stream);
+
 /* adjoint_reconstruct (solver.py:363-406): image = allreduce(F^H d). */
 int csr_adjoint_reconstruct(csr_plan *plan, const void *kdata, void *image,
                             void *stream);

@@ -8,7 +8,8 @@ a C ABI, include/csrecon_b200.h); PyTorch only provides device memory and
 streams.  There is no CPU fallback.
 """
 
-from .acquisition import ImageGrid, KSpaceDataset, SensitivityMaps, Trajectory
+from .acquisition import (ImageGrid, KSpaceDataset, SensitivityMaps, Trajectory,
+                          simulate_kspace)
 from .errors import (CgDivergenceError, MemoryBudgetError, NativeError,
                      ShapeMismatchError, SpmdError)
 from .operators import (DEFAULT_MEMORY_BUDGET, DftFactors, DftOperator,
@@ -32,7 +33,7 @@ def active_backend():
 
 
 __all__ = [
-    "ImageGrid", "KSpaceDataset", "SensitivityMaps", "Trajectory",
+    "ImageGrid", "KSpaceDataset", "SensitivityMaps", "Trajectory", "simulate_kspace",
     "CgDivergenceError", "MemoryBudgetError", "NativeError", "ShapeMismatchError",
     "SpmdError", "DEFAULT_MEMORY_BUDGET", "DftFactors", "DftOperator",
     "build_factors", "CommStats", "ShardPlan", "coil_shard_plan",

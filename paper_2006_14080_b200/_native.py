@@ -80,6 +80,7 @@ SIGNATURES = {
     "csr_plan_set_timing": [_P, _P, _I64, _P],
     "csr_plan_kernel_times": [_P, _P, _P, _P, _P],
     "csr_plan_probe": [_P, _I32, _P, _P],
+    "csr_simulate_kspace": [_I32, _I32, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "csr_adjoint_reconstruct": [_P, _P, _P, _P],
     "csr_comm_unique_id": [_P],
     "csr_comm_create": [_P, _I32, _I32, _I32, ctypes.POINTER(_P)],

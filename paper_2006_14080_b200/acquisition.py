@@ -123,3 +123,37 @@ def sample_coords(trajectory):
         if coords.ndim != 2 or coords.shape[1] != 2:
             raise ValueError(f"coords must have shape (n, 2), got {coords.shape}")
     return np.asarray(coords, dtype=np.float64)
+
+
+def simulate_kspace(image, sens, trajectory, n_frames=1, device=None):
+    """Direct multi-coil encoding in double precision on the GPU
+    (acquisition.py:233-257): d[k, c] = sum_n s_c[n] image[n] exp(-2 pi i
+    k_k . r_n), pixels on the centred integer grid, no normalisation.  For
+    2-D+t pass image (T, nx, ny) and a trajectory of T*M rows (frame-major).
+    Returns a KSpaceDataset with complex128 samples."""
+    from . import _dev, _native
+    maps = np.asarray(getattr(sens, "maps", sens))
+    img = np.asarray(image)
+    frames = img.reshape((-1,) + img.shape[-2:]) if img.ndim == 3 else img[None]
+    if frames.shape[1:] != maps.shape[1:]:
+        raise ValueError(f"image shape {img.shape} != sensitivity grid {maps.shape[1:]}")
+    T = frames.shape[0]
+    if img.ndim == 3 and T != n_frames:
+        n_frames = T
+    coords = sample_coords(trajectory)
+    if coords.shape[0] % T:
+        raise ValueError("trajectory rows must split evenly into the image frames")
+    M = coords.shape[0] // T
+    dev = device if device is not None else _dev.device_of()
+    torch = _dev.torch
+    c = torch.from_numpy(np.ascontiguousarray(coords)).to(dev)
+    s = torch.from_numpy(np.ascontiguousarray(maps.astype(np.complex128))).to(dev)
+    x = torch.from_numpy(np.ascontiguousarray(frames.astype(np.complex128))).to(dev)
+    out = torch.empty((T * M, maps.shape[0]), dtype=torch.complex128, device=dev)
+    _native.call("csr_simulate_kspace", maps.shape[1], maps.shape[2], T, maps.shape[0], M,
+                 c.data_ptr(), s.data_ptr(), x.data_ptr(), out.data_ptr(),
+                 _dev.stream_ptr(dev))
+    data = out.cpu().numpy()
+    traj = trajectory if isinstance(trajectory, Trajectory) else \
+        Trajectory(coords, coords.shape[0], 1)
+    return KSpaceDataset(data, traj, n_frames=T)

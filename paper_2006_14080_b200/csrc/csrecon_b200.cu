@@ -20,6 +20,7 @@
 #include "nudft_simt.cuh"
 #include "nudft_tc.cuh"
 #include "cg_tail.cuh"
+#include "simulate.cuh"
 
 using namespace csr;
 
@@ -876,6 +877,24 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
 int csr_debug_trace(csr_plan *p, unsigned long long *host, int64_t n) {
     if (!p || !p->tc.trace) return fail(CSR_ERR_ARG, "no trace buffer (set CSR_TRACE)");
     CU(cudaMemcpy(host, p->tc.trace, std::min<int64_t>(n, 4096 * 32) * 8, cudaMemcpyDeviceToHost));
+    return CSR_OK;
+}
+
+int csr_simulate_kspace(int32_t nx, int32_t ny, int32_t n_frames, int32_t n_coils,
+                        int64_t n_samples, const double *coords, const void *sens,
+                        const void *image, void *kspace, void *stream) {
+    if (!coords || !sens || !image || !kspace) return fail(CSR_ERR_ARG, "null argument");
+    if (nx < 1 || ny < 1 || n_frames < 1 || n_coils < 1 || n_samples < 1)
+        return fail(CSR_ERR_SHAPE, "dimensions must all be >= 1");
+    if (n_coils > 65535 || n_frames > 65535) return fail(CSR_ERR_SHAPE, "too many coils / frames");
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    TRY(check_device(dev));
+    dim3 grid((unsigned)((n_samples + SIM_T - 1) / SIM_T), (unsigned)n_coils, (unsigned)n_frames);
+    CU(launch(k_simulate_f64, grid, dim3(256), 0, (cudaStream_t)stream, coords,
+              (const double2 *)sens, (const double2 *)image, (double2 *)kspace, n_samples, nx, ny,
+              n_coils));
+    LAUNCHED();
     return CSR_OK;
 }
 
