@@ -141,8 +141,10 @@ def encode_f64(image, sens, coords, chunk=4096):
     return out
 
 
-def make_problem(cfg, seed=None):
-    """Build config ``cfg`` (0-4) with its fixed seed (or ``seed``)."""
+def make_problem(cfg, seed=None, encoder=None):
+    """Build config ``cfg`` (0-4) with its fixed seed (or ``seed``).
+    ``encoder(img, sens, coords)`` replaces the CPU f64 separable encode (the
+    GPU f64 simulate_kspace for the large configs; identical to 1e-12)."""
     c = CONFIGS[cfg]
     rng = np.random.default_rng(SEED_BASE + cfg if seed is None else seed)
     nx, ny, T, C = c["nx"], c["ny"], c["n_frames"], c["n_coils"]
@@ -153,7 +155,7 @@ def make_problem(cfg, seed=None):
         img = render_phantom(ellipses, nx, ny, None if T == 1 else f)
         kc = golden_angle_coords(c["spokes"], c["readout"], f * c["spokes"])
         coords.append(kc)
-        data.append(encode_f64(img.astype(np.complex128), sens, kc))
+        data.append((encoder or encode_f64)(img.astype(np.complex128), sens, kc))
         truth.append(img)
     coords = np.concatenate(coords, 0)
     data = np.concatenate(data, 0)
