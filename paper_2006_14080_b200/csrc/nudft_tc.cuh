@@ -1214,6 +1214,12 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         }
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tr[28] = gtimer();
+        tr[29] = smid;
+    }
     if (run) probe_exit(P.probe);
     if (warp == 1) {
         tc_fence_after();
