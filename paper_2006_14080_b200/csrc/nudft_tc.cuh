@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         }
         for (int r = 0; r < NR; ++r) {
             mbar_init(&rfull[r], 1);
-            mbar_init(&dfull[r], 1);
+            mbar_init(&dfull[r], 2);
             mbar_init(&rempty[r], ADJ_GW);
         }
         mbar_init(acc_full, 1);
@@ -1004,7 +1004,9 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
         if (warp == 0 && lane == 0)
             for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0);
     } else if (warp == 0) {
-        // ---- B ring producer: conj(P1)^T hi / lo tiles
+        // ---- lane 0: B ring producer (conj(P1)^T hi / lo tiles); lane 1:
+        // input ring producer (P0 rows of the tile's x values, and d).  Both
+        // are single-thread loops that mostly sleep on their barriers.
         if (lane == 0) {
             for (int i = pre; i < nkb; ++i) {
                 const int kb = kb0 + i;
@@ -1015,10 +1017,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
                 tma_load_2d(st + ADJ_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
             }
-        }
-    } else if (warp == 2) {
-        // ---- input ring producer: P0 rows of the tile's x values, and d
-        if (lane == 0) {
+        } else if (lane == 1) {
             const uint32_t tx = P.raw_bytes;
             for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
                 const int kb = kb0 + i;
@@ -1033,8 +1032,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 3) {
-        // ---- input prep: d' = sg * ((dr, di), (di, -dr)) per (k, c)
+    } else if (warp == 2 || warp == 3) {
+        // ---- input prep, split between two sub-partitions (one warp would
+        // make its sub-partition's generator the straggler):
+        // d' = sg * ((dr, di), (di, -dr)) per (k, c)
         const float sg = pow2_scale(P.scales[5]);
         for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
             wait_slow(&rfull[r], rph);
@@ -1042,7 +1043,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             const float2 *d = reinterpret_cast<const float2 *>(in + OFF_D);
             float4 *dp = reinterpret_cast<float4 *>(in + OFF_DP);
 #pragma unroll
-            for (int e = lane; e < 32 * CP; e += 32) {
+            for (int e = (warp - 2) * 32 + lane; e < 32 * CP; e += 64) {
                 const float2 v = d[e];
                 dp[e] = make_float4(sg * v.x, sg * v.y, sg * v.y, -sg * v.x);
             }
@@ -1110,7 +1111,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             const float2 *p0s = reinterpret_cast<const float2 *>(in);
             const float2 *dps = reinterpret_cast<const float2 *>(in + OFF_DP) + (c * 2 + part);
             uint32_t hv[ADJ_SPW], lv[ADJ_SPW];
-            if (P.exp_flags & 1) {
+            if ((P.exp_flags & 1) || ((P.exp_flags & (2048 << q)) != 0)) {
 #pragma unroll
                 for (int k = 0; k < ADJ_SPW; ++k) hv[k] = lv[k] = 0u;
             } else

@@ -33,9 +33,9 @@ __device__ __forceinline__ void wait_mode(int wm, uint64_t *bar, uint32_t parity
 
 __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out, int burn,
                        int smsp_mask, int PW, int MW, int nowait, int yield_every) {
-    const int wm = mode / 10;
-    mode %= 10;
-    __shared__ __align__(1024) uint8_t tile[16384];
+    const int wm = mode / 100;
+    mode %= 100;
+    __shared__ __align__(1024) uint8_t tile[40960];
     __shared__ uint64_t full[8], empty[8];
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -44,7 +44,7 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out,
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        if (mode % 10 == 5) mbar_init(&empty[1], (1 << 20) - 1);
+        if (mode == 5) mbar_init(&empty[1], (1 << 20) - 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(&tslot, 512);
@@ -53,7 +53,7 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out,
     tc_fence_after();
     const uint32_t tmem = tslot;
     const unsigned long long t0 = clock64();
-    if (mode >= 5) {  // single-thread primitive throughput
+    if (mode >= 5 && mode <= 7) {  // single-thread primitive throughput
         if (threadIdx.x == 0) {
             uint64_t *b = &full[0];
             if (mode == 5) {  // arrive only (barrier expects far more)
@@ -127,6 +127,12 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out,
             } else if (mode == 8) {  // 4 into hi, then 8 into lo
                 for (int k = 0; k < 12; ++k)
                     mma_f16_ts(tmem + (k < 4 ? 0 : 128), tmem + 256 + 8 * (k & 3), bd + 2 * (k & 3), idesc, 1);
+            } else if (mode == 10) {  // M=128 N=64: 24 MMAs (same MACs)
+                for (int k = 0; k < 24; ++k)
+                    mma_f16_ts(tmem, tmem + 256 + 8 * (k & 3), bd + 2 * (k & 3), idesc_f16(128, 64), 1);
+            } else if (mode == 11) {  // SS N=256, 6 MMAs
+                for (int k = 0; k < 6; ++k)
+                    mma_f16(tmem, bd + 2 * (k & 3), bd + 2 * (k & 3), idesc_f16(128, 256), 1);
             } else if (mode == 9) {  // N=256 single accumulator, 6 MMAs (same MACs)
                 for (int k = 0; k < 6; ++k)
                     mma_f16_ts(tmem, tmem + 256 + 8 * (k & 3), bd + 2 * (k & 3), idesc_f16(128, 256), 1);
@@ -144,7 +150,7 @@ __global__ void k_pipe(int mode, int iters, int stages, unsigned long long *out,
     }
     __syncthreads();
     const unsigned long long t1 = clock64();
-    if (threadIdx.x == 0 && mode >= 5) out[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0 && mode >= 5 && mode <= 7) out[blockIdx.x] = t1 - t0;
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -156,11 +162,11 @@ int main() {
     cudaMalloc(&d, sizeof(h));
     const char *names[] = {"plain arrive", "commit only", "12 MMA TS + commit", "12 MMA SS + commit",
                            "12 TS hi/lo/lo", "1T arrive", "1T try_wait done", "1T arrive+wait",
-                           "12 TS 4hi+8lo", "6 TS N=256"};
-    for (int mode : {2}) {
-      for (int burn : {64}) {
-       for (int nthr : {512}) {
-        for (int pm : {0x01, 0x10001, 0x20001, 0x40001, 0x80001}) {
+                           "12 TS 4hi+8lo", "6 TS N=256", "24 TS N=64", "6 SS N=256"};
+    for (int mode : {2, 9, 10, 3, 11}) {
+      for (int burn : {0}) {
+       for (int nthr : {128}) {
+        for (int pm : {0x01}) {
             const int PW = (pm >> 4) & 15, MW = pm & 15, mask = ((pm >> 12) & 15) ? 0xd : 0xf;
             const int nowait = (pm >> 8) & 3;
             const int iters = 2000, stages = 4;
@@ -175,7 +181,7 @@ int main() {
             double avg = 0;
             for (int i = 0; i < 148; ++i) avg += h[i];
             avg /= 148;
-            printf("%-22s burn=%2d threads=%d mask=%x nowait=%d yield=%d  %8.1f cycles/iter\n", names[mode % 10], burn, nthr, mask, nowait, yield_every, avg / iters);
+            printf("%-22s burn=%2d threads=%d mask=%x nowait=%d yield=%d  %8.1f cycles/iter\n", names[mode % 100], burn, nthr, mask, nowait, yield_every, avg / iters);
         }
        }
       }
