@@ -294,8 +294,8 @@ def run_ours(args, cfg, world, rank, local):
     kt = {"forward": fm.value, "adjoint": am.value}
     kn = {"forward": fn.value, "adjoint": an.value}
     breakdown = {}
-    for slot, name in enumerate(["forward", "adjoint", "admm_mu", "admm_rhs", "operand_prep",
-                                 "cg_tail", "admm_post"]):
+    for slot, name in enumerate(["forward", "adjoint", "admm_head_or_mu", "admm_rhs",
+                                 "operand_prep", "cg_tail", "admm_post"]):
         ms_, n_ = ctypes.c_double(), ctypes.c_int64()
         _native.call("csr_plan_probe", op.plan, slot, ctypes.byref(ms_), ctypes.byref(n_))
         if n_.value:

@@ -109,6 +109,41 @@ __device__ __forceinline__ void all_totals(const double *part, double (&tot)[NV]
 #define TAIL_STAMP(i) \
     if (A.stamps && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
     A.stamps[(blockIdx.x ? 16 : 0) + (i)] = gtimer()
+// the forward's fp16 hi/lo operand for pixel (t, x, y) of image value v:
+// rows (x, c, Re/Im) doubled, sigma * s_c * v (k_tc_prep_x, valid entries only;
+// the zero padding is written once at plan build)
+__device__ __forceinline__ void write_x_operand(const CgTailArgs &A, int t, int xx, int y,
+                                                int64_t nxy, float2 v, float sg) {
+    const TcArgs &a = A.a;
+    const int hy = a.Kf / 2;
+    uint32_t *H = reinterpret_cast<uint32_t *>(A.xb_hi);
+    uint32_t *L = reinterpret_cast<uint32_t *>(A.xb_lo);
+    const int64_t p = (int64_t)xx * A.g.ny + y;
+    for (int c0 = 0; c0 < a.C; c0 += 8) {
+        float2 sv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            sv[j] = c0 + j < a.C ? A.sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = c0 + j;
+            if (c >= a.C) break;
+            float2 w = cmul(sv[j], v);
+            w.x *= sg;
+            w.y *= sg;
+            __half rh, rl, ih, il;
+            split16(w.x, rh, rl);
+            split16(w.y, ih, il);
+            const int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)xx * a.Cp + c);
+            const int64_t e = row * hy + y, e1 = e + hy;
+            H[e] = pack2(rh, hneg(ih));
+            L[e] = pack2(rl, hneg(il));
+            H[e1] = pack2(ih, rh);
+            L[e1] = pack2(il, rl);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
@@ -240,43 +275,137 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
     const float dbound = rmax_all + fabsf(be) * dbound_old;
     const float sg = pow2_scale(2.f * A.scales[4] * dbound);
     if (blockIdx.x == 0 && threadIdx.x == 0) A.scales[5] = 0.f;  // forward atomicMax
-    const TcArgs &a = A.a;
-    const int hy = a.Kf / 2;
-    uint32_t *H = reinterpret_cast<uint32_t *>(A.xb_hi);
-    uint32_t *L = reinterpret_cast<uint32_t *>(A.xb_lo);
     for (int64_t i = i0; i < g.n; i += stride) {
         const float2 d = b.d[i], r = b.r[i];
         const float2 nd = make_float2(r.x + be * d.x, r.y + be * d.y);
         b.d[i] = nd;
         int t, xx, y;
         unflat(g, i, t, xx, y);
-        const int64_t p = (int64_t)xx * g.ny + y;
-        for (int c0 = 0; c0 < a.C; c0 += 8) {
-            float2 sv[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                sv[j] = c0 + j < a.C ? A.sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int c = c0 + j;
-                if (c >= a.C) break;
-                float2 v = cmul(sv[j], nd);
-                v.x *= sg;
-                v.y *= sg;
-                __half rh, rl, ih, il;
-                split16(v.x, rh, rl);
-                split16(v.y, ih, il);
-                const int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)xx * a.Cp + c);
-                const int64_t e = row * hy + y, e1 = e + hy;
-                H[e] = pack2(rh, hneg(ih));
-                L[e] = pack2(rl, hneg(il));
-                H[e1] = pack2(ih, rh);
-                L[e1] = pack2(il, rl);
-            }
-        }
+        write_x_operand(A, t, xx, y, nxy, nd, sg);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
     TAIL_STAMP(7);
+    probe_exit(A.probe);
+}
+
+
+// ADMM iteration head (single rank, tensor-core operator): k_admm_mu +
+// k_admm_rhs + the first forward's k_tc_prep_x in one cooperative kernel
+// (solver.py:178-183, 99-108):
+//   phase 1  mu+ = S(theta(rho) + eta)
+//   barrier  (the rhs stencil reads mu at neighbouring pixels)
+//   phase 2  rhs = fhd + (beta/2) Theta^H (mu - eta); x = 0; r = d = rhs;
+//            ||r||^2 and max|rhs| partials
+//   barrier  tau, CG activation (fin_rhs), sigma_x from the exact max
+//   phase 3  the forward operand of d
+__global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
+    pdl_enter();
+    const Geom &g = A.g;
+    const AdmmBufs &b = A.b;
+    DevScalars *s = b.s;
+    if (!s->admm_active) return;  // uniform
+    probe_enter(A.probe);
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const int cur = s->cur, cg_max = s->cg_max;
+    const double atol2 = s->atol2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    __shared__ unsigned gen0;
+    if (threadIdx.x == 0) gen0 = grid_gen(A.bar);
+    // ---- phase 1: mu
+    {
+        const float2 *rho = b.rho[cur];
+        for (int64_t i = i0; i < g.n * g.D; i += stride) {
+            const int comp = (int)(i / g.n);
+            int t, x, y;
+            unflat(g, i - comp * g.n, t, x, y);
+            const float2 v = cadd(theta_at(rho, g, comp, t, x, y, nullptr), b.eta[i]);
+            b.mu[i] = soft1(v, comp == 2 ? b.t_t : b.t_s);
+        }
+    }
+    grid_barrier(A.bar, gen0 + 1);
+    // ---- phase 2: rhs and the zero-start CG state
+    {
+        float2 *x = b.rho[cur ^ 1];
+        MuMinusEta u{b.mu, b.eta, g, nullptr};
+        double v[1] = {0.0};
+        float dmax = 0.f;
+        for (int64_t i = i0; i < g.n; i += stride) {
+            int t, xx, y;
+            unflat(g, i, t, xx, y);
+            const float2 l = theta_adj_at(u, g, t, xx, y);
+            const float2 f = b.fhd[i];
+            const float2 rhs = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+            x[i] = make_float2(0.f, 0.f);
+            b.r[i] = rhs;
+            b.d[i] = rhs;
+            v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
+            dmax = fmaxf(dmax, fmaxf(fabsf(rhs.x), fabsf(rhs.y)));
+        }
+        __shared__ float shm[32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        if (lane == 0) shm[warp] = dmax;
+        block_partials<1>(v, A.part);  // slot 0 (syncs the block)
+        if (warp == 0) {
+            float w = lane < (int)(blockDim.x >> 5) ? shm[lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+            if (lane == 0) A.part[1 * (size_t)gridDim.x + blockIdx.x] = w;
+        }
+    }
+    grid_barrier(A.bar, gen0 + 2);
+    double tau;
+    float dmax_all;
+    {
+        __shared__ double r_tau;
+        __shared__ float r_max;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (warp == 0) {
+            double w = 0.0;
+            float m = 0.f;
+            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
+                w += __ldcg(A.part + bb);
+                m = fmaxf(m, (float)__ldcg(A.part + gridDim.x + bb));
+            }
+            w = warp_sum(w);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) {
+                r_tau = w;
+                r_max = m;
+            }
+        }
+        __syncthreads();
+        tau = r_tau;
+        dmax_all = r_max;
+    }
+    // fin_rhs (solver.py:106-108), every block identically
+    const bool finite = isfinite(tau);
+    const bool go = finite && cg_max > 0 && tau > atol2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s->tau = tau;
+        s->cg_iter = 0;
+        if (!finite) {
+            s->error = 1;
+            s->cg_active = 0;
+            s->admm_active = 0;
+        } else {
+            s->cg_active = go ? 1 : 0;
+        }
+        A.scales[5] = 0.f;  // the forward's max|kd| (atomicMax)
+        A.scales[6] = dmax_all;
+    }
+    // ---- phase 3: the first forward's operand of d = rhs
+    if (go) {
+        const float sg = pow2_scale(2.f * A.scales[4] * dmax_all);
+        for (int64_t i = i0; i < g.n; i += stride) {
+            int t, xx, y;
+            unflat(g, i, t, xx, y);
+            write_x_operand(A, t, xx, y, nxy, b.d[i], sg);
+        }
+    }
     probe_exit(A.probe);
 }
 

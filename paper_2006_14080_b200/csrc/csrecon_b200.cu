@@ -302,7 +302,7 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
 // One ADMM iteration as a fixed kernel sequence (captured as a graph).
 // The fused CG tail (cg_tail.cuh) on a single rank with the tensor-core
 // operator; multi-rank and SIMT runs keep the separate kernels.
-int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
+int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = false) {
     if (!p->tail_blocks) {
         int per_sm = 0, sms = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail, TPB, 0));
@@ -323,7 +323,7 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
     A.scales = p->tc.scales;
     A.part = p->tail_part;
     A.bar = p->tickets + 8;
-    A.probe = p->tc.probe ? p->tc.probe + 4 * PROBE_TAIL : nullptr;
+    A.probe = p->tc.probe ? p->tc.probe + 4 * (head ? PROBE_MU : PROBE_TAIL) : nullptr;
     A.stamps = p->tc.trace ? p->tc.trace + 100000 : nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)p->tail_blocks);
@@ -334,8 +334,14 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, k_cg_tail, A));
+    CU(cudaLaunchKernelEx(&cfg, head ? k_admm_head : k_cg_tail, A));
     LAUNCHED();
+    return CSR_OK;
+}
+
+// ADMM head (mu + rhs + first forward operand), same conditions as the tail
+int launch_admm_head(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
+    TRY(launch_cg_tail(p, b, st, true));
     return CSR_OK;
 }
 
@@ -373,17 +379,22 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
         launch(k_stage_frames, ebf, TPB, 0, st, b, g, 0, p->sfirst, p->slast); LAUNCHED(); ++k;
         TRY(halo_exchange(p, p->sfirst, p->slast, st));
     }
-    launch(k_admm_mu, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
-    if (fm) TRY(halo_exchange(p, p->sfirst, p->sfirst, st));  // next rank's (mu-eta)_t[0]
-    launch(k_admm_rhs, eb, TPB, 0, st, g, b); LAUNCHED(); ++k;
-    TRY(scalar_sync(p, b, FIN_RHS, 0, 1, st, &k));
+    const bool tail = use_cg_tail(p);
+    if (tail) {  // one cooperative kernel: mu, rhs, CG init, first operand
+        TRY(launch_admm_head(p, b, st));
+        ++k;
+    } else {
+        launch(k_admm_mu, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
+        if (fm) TRY(halo_exchange(p, p->sfirst, p->sfirst, st));  // next rank's (mu-eta)_t[0]
+        launch(k_admm_rhs, eb, TPB, 0, st, g, b); LAUNCHED(); ++k;
+        TRY(scalar_sync(p, b, FIN_RHS, 0, 1, st, &k));
+    }
     const int *gate = &p->sc->cg_active;
     const bool coil_multi = !fm && p->comm && p->comm->nranks > 1;
     const int64_t nf = (int64_t)g.nx * g.ny;
-    const bool tail = use_cg_tail(p);
     for (int it = 0; it < cg_max; ++it) {
         if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
-        const bool x_ready = tail && it > 0;  // the previous tail wrote X
+        const bool x_ready = tail;  // the head / previous tail wrote X
         TRY(run_forward(p, p->d, nullptr, st, gate, true, x_ready));
         k += p->tc.enabled ? tc_forward_launches(p->tc, true, false, x_ready) : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));

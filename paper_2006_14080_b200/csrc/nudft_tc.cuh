@@ -1408,6 +1408,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     TCA(tc.p0p, (size_t)T * tc.Mk * tc.nxp * 8, factor_bytes);
     TCA(tc.xb_hi, xb * 2, ws_bytes);
     TCA(tc.xb_lo, xb * 2, ws_bytes);
+    // zero padding rows / columns once: the fused loop kernels write only
+    // the valid (x < nx, c < C, y < ny) entries of the operand
+    cudaMemsetAsync(tc.xb_hi, 0, xb * 2, st);
+    cudaMemsetAsync(tc.xb_lo, 0, xb * 2, st);
     TCA(tc.kdp, (size_t)G * T * tc.Mk * Cp * 8, ws_bytes);
     TCA(tc.kdi, (size_t)T * tc.Mk * Cp * 8, ws_bytes);
     cudaMemsetAsync(tc.kdi, 0, (size_t)T * tc.Mk * Cp * 8, st);
