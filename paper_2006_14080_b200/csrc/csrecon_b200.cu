@@ -174,7 +174,7 @@ int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
                 const int *gate, bool in_loop = false, bool x_ready = false) {
     if (p->tc.enabled) {
         if (tc_forward(p->tc, x, out, st, gate, in_loop, x_ready))
-            return fail(CSR_ERR_CUDA, "tc forward launch");
+            return fail(CSR_ERR_CUDA, "tc forward launch: " + tc_last_error());
         g_launches.fetch_add(tc_forward_launches(p->tc, in_loop, out != nullptr, x_ready),
                              std::memory_order_relaxed);
         return CSR_OK;
@@ -191,7 +191,7 @@ int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
 int run_adjoint_partials(csr_plan *p, const float2 *kd, cudaStream_t st,
                          const int *gate) {
     if (p->tc.enabled) {
-        if (tc_adjoint(p->tc, kd, p->ws, st, gate)) return fail(CSR_ERR_CUDA, "tc adjoint launch");
+        if (tc_adjoint(p->tc, kd, p->ws, st, gate)) return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
         g_launches.fetch_add(p->tc.adj_launches + (kd ? 1 : 0), std::memory_order_relaxed);
         return CSR_OK;
     }

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -69,8 +70,14 @@ struct TcPlan {
     double *red = nullptr;
     unsigned *tick = nullptr;
     CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
-    CUtensorMap tm_xb128_hi, tm_xb128_lo;
+    CUtensorMap tm_xb256_hi, tm_xb256_lo;
 };
+
+// last CUDA error string of a failed tensor-core launch (for csr_last_error)
+inline std::string &tc_last_error() {
+    static thread_local std::string e;
+    return e;
+}
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -406,28 +413,30 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
 }
 
 // Forward, A-stationary form (2*nyp <= 256), persistent.  The work is the
-// list of (sample tile m, N tile n) units, m-major; CTA b of the grid (one
-// per SM) takes the contiguous range [b*U/G, (b+1)*U/G), i.e. one or more
-// segments of N tiles of consecutive sample tiles.  Per segment the 128
-// samples' P1 rows (A, fp16 hi/lo) are loaded into TMEM once (from the
-// lane-major copy of the factor: fully coalesced) while the image operand
-// X' (B, 128 doubled rows = 64 complex (x, c) columns per tile) streams
-// through a TMA ring; MMAs read A from TMEM and only B from shared memory.
-// Double-buffered accumulators (N = 128) let the row-dot epilogue of tile j
-// overlap the MMAs of tile j+1.  A sample tile split across CTAs leaves one
-// partial per piece; the last piece to finish (ticket) sums them in piece
-// order, so the result does not depend on timing.
-//   TMEM: [0,128) A_hi, [128,256) A_lo, [256,384) / [384,512) accumulators.
+// list of (sample tile m, N tile n) units, m-major, with N tiles of 256
+// doubled image rows (128 complex (x, c) columns): one N = 256 MMA per K
+// step and operand runs at ~3300 MACs/clk/SM against ~2700 for N = 128
+// (tools/pipe_micro.cu).  CTA b of the grid (one per SM) takes the
+// contiguous range [b*U/G, (b+1)*U/G), i.e. one or more segments of N tiles
+// of consecutive sample tiles.  Per segment the 128 samples' P1 rows (A,
+// fp16 hi/lo) are loaded into TMEM once (lane-major copy: coalesced) while
+// the image operand X' streams through a TMA ring; MMAs read A from TMEM
+// and only B from shared memory.  The single 256-column accumulator is
+// drained by sixteen epilogue warps (four per TMEM lane quarter, one per
+// 64-column quarter) straight into registers, so the tensor core waits only
+// for the TMEM reads; the row-dot `kd[k,c] += sum_x P0[k,x] G[k,(x,c)]`
+// runs after the release.  A sample tile split across CTAs leaves one
+// partial per piece; the CTA holding piece 0 sums pieces in order.
+//   TMEM: [0,128) A_hi, [128,256) A_lo, [256,512) accumulator.
 constexpr int FTS_STAGES = 3;
-constexpr int FTS_KPS = 2;             // K blocks per pipeline stage
-constexpr int FTS_B_TILE = 128 * 128;  // 16 KiB per hi / lo per K block
-constexpr int FTS_THREADS = 192;       // TMA, MMA, 4 epilogue (+A loader) warps
+constexpr int FTS_B_TILE = 256 * 128;  // 32 KiB per hi / lo per K block (256 rows)
+constexpr int FTS_THREADS = 576;       // TMA, MMA, 16 epilogue (+A loader) warps
 
 struct FwdTsParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
     TcArgs a;
     int mt_per_frame;
-    int nt_tiles;    // N tiles per sample tile (Nf / 128)
+    int nt_tiles;    // 256-row N tiles per sample tile (Nf / 256)
     int64_t units;   // T * mt_per_frame * nt_tiles
     const uint4 *fa_hi, *fa_lo;  // lane-major: [mtile][Kf/8][128 rows] x 16 B
     const float2 *p0p;
@@ -459,18 +468,18 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     // barrier init, TMEM allocation and the first segment's A rows read only
     // static data; everything else waits in pdl_wait().
     pdl_trigger();
-    constexpr int XS = 64 / CP;  // x values per 128-row B tile
+    constexpr int XQ = 32 / CP;  // x values per 64-column accumulator quarter
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    constexpr int STAGE = FTS_KPS * 2 * FTS_B_TILE;
-    const int kps = (P.a.Kf / 64) % FTS_KPS == 0 ? FTS_KPS : 1;
+    constexpr int STAGE = 2 * FTS_B_TILE;  // one K block: [hi | lo] x 256 rows
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + FTS_STAGES * STAGE);
     uint64_t *empty = full + FTS_STAGES;
     uint64_t *tfull = empty + FTS_STAGES;
-    uint64_t *tempty = tfull + 2;
-    uint64_t *a_ready = tempty + 2;
+    uint64_t *tempty = tfull + 1;
+    uint64_t *a_ready = tempty + 1;
     uint64_t *a_free = a_ready + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_free + 1);
+    __shared__ float2 part_acc[128][CP + 1];  // row sums folded across the quarters
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x;
@@ -488,11 +497,9 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
-        }
-        mbar_init(a_ready, 4);
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 16);
+        mbar_init(a_ready, 16);
         mbar_init(a_free, 1);
         fence_barrier_init();
     }
@@ -503,33 +510,24 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
-    // A rows of sample tile m -> TMEM (epilogue warps; lane = sample row).
-    // Lane-major factor copy: every load of a warp is 512 contiguous bytes;
-    // 16 chunks (hi + lo) in flight per thread per round.
+    // A rows of sample tile m -> TMEM: the four epilogue warps of a lane
+    // quarter split the row (part 0/1: hi columns, 2/3: lo columns; 16
+    // chunks in flight per thread).  Lane-major factor copy: 512 contiguous
+    // bytes per warp load.
     const int nchunk = P.a.Kf / 8;  // 16-byte column chunks per row (hi or lo)
-    auto load_a = [&](int64_t m, uint32_t lane_base, int row) {
-        const uint4 *gh = P.fa_hi + (size_t)m * nchunk * 128 + row;
-        const uint4 *gl = P.fa_lo + (size_t)m * nchunk * 128 + row;
-        for (int c0 = 0; c0 < nchunk; c0 += 16) {
-            uint4 h[16], l[16];
+    auto load_a = [&](int64_t m, uint32_t lane_base, int row, int part) {
+        const uint4 *g = ((part >> 1) ? P.fa_lo : P.fa_hi) + (size_t)m * nchunk * 128 + row;
+        const int half = nchunk / 2;  // chunks per part (Kf = 2*nyp, multiple of 64)
+        const int c0 = (part & 1) * half;
+        const uint32_t dst = lane_base + ((part >> 1) ? 128 : 0);
+        for (int cc = 0; cc < half; cc += 8) {
+            uint32_t vh[32];
 #pragma unroll
-            for (int v = 0; v < 16; ++v) {
-                h[v] = c0 + v < nchunk ? __ldg(gh + (size_t)(c0 + v) * 128) : make_uint4(0, 0, 0, 0);
-                l[v] = c0 + v < nchunk ? __ldg(gl + (size_t)(c0 + v) * 128) : make_uint4(0, 0, 0, 0);
+            for (int v = 0; v < 8; ++v) {
+                const uint4 a = __ldg(g + (size_t)(c0 + cc + v) * 128);
+                vh[4 * v] = a.x; vh[4 * v + 1] = a.y; vh[4 * v + 2] = a.z; vh[4 * v + 3] = a.w;
             }
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                if (c0 + 8 * half >= nchunk) break;
-                uint32_t vh[32], vl[32];
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    const uint4 a = h[8 * half + v], b = l[8 * half + v];
-                    vh[4 * v] = a.x; vh[4 * v + 1] = a.y; vh[4 * v + 2] = a.z; vh[4 * v + 3] = a.w;
-                    vl[4 * v] = b.x; vl[4 * v + 1] = b.y; vl[4 * v + 2] = b.z; vl[4 * v + 3] = b.w;
-                }
-                tmem_st32(lane_base + (c0 + 8 * half) * 4, vh);
-                tmem_st32(lane_base + 128 + (c0 + 8 * half) * 4, vl);
-            }
+            tmem_st32(dst + (c0 + cc) * 4, vh);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -538,7 +536,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     };
     if (warp >= 2 && u0 < u1) {
         const int q = warp & 3;
-        load_a(u0 / NT, tmem + ((uint32_t)(q * 32) << 16), q * 32 + lane);
+        load_a(u0 / NT, tmem + ((uint32_t)(q * 32) << 16), q * 32 + lane, (warp - 2) >> 2);
         if (tr && threadIdx.x == 64) tr[5] = gtimer();
     }
 
@@ -555,19 +553,16 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                 const int64_t m = u / NT;
                 const int nt = (int)(u - m * NT);
                 const int t = (int)(m / P.mt_per_frame);
-                const int brow = t * P.a.Nf + nt * 128;
-                for (int kb = 0; kb < nkb; kb += kps, ++it) {
+                const int brow = t * P.a.Nf + nt * 256;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % FTS_STAGES;
                     const uint32_t ph = (it / FTS_STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t *st = smem + s * STAGE;
-                    mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : kps * 2 * FTS_B_TILE);
+                    mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : STAGE);
                     if (!(P.exp_flags & 2)) {
-                        for (int v = 0; v < kps; ++v) {
-                            uint8_t *sb = st + v * 2 * FTS_B_TILE;
-                            tma_load_2d(sb, &tmB_hi, &full[s], (kb + v) * 64, brow);
-                            tma_load_2d(sb + FTS_B_TILE, &tmB_lo, &full[s], (kb + v) * 64, brow);
-                        }
+                        tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
+                        tma_load_2d(st + FTS_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
                     }
                 }
             }
@@ -575,8 +570,8 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     } else if (warp == 1) {
         // ---- MMA issuer
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(128, 128);
-            const uint32_t a_hi = tmem, a_lo = tmem + 128;
+            constexpr uint32_t idesc = idesc_f16(128, 256);
+            const uint32_t a_hi = tmem, a_lo = tmem + 128, dcol = tmem + 256;
             int it = 0, tc = 0, seg = 0;
             int64_t m_prev = -1;
             for (int64_t u = u0; u < u1; ++u, ++tc) {
@@ -589,75 +584,45 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     ++seg;
                     m_prev = m;
                 }
-                const int ab = tc & 1;
-                const uint32_t aph = (tc >> 1) & 1;
-                mbar_wait(&tempty[ab], aph ^ 1);
+                mbar_wait(tempty, (tc & 1) ^ 1);  // the epilogue has read the last unit
                 tc_fence_after();
-                const uint32_t dcol = tmem + 256 + ab * 128;
-                for (int kb = 0; kb < nkb; kb += kps, ++it) {
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % FTS_STAGES;
                     const uint32_t ph = (it / FTS_STAGES) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    for (int v = 0; v < kps; ++v) {
-                        const uint32_t st = smem_u32(smem + s * STAGE + v * 2 * FTS_B_TILE);
+                    const uint32_t st = smem_u32(smem + s * STAGE);
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint32_t ac = (kb + v) * 32 + kk * 8;
-                            const uint64_t dbh = desc_sw128(st + kk * 32);
-                            const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
-                            if (P.exp_flags & 1) continue;
-                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, ((kb + v) | kk) != 0);
-                            mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
-                            mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
-                        }
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t ac = kb * 32 + kk * 8;
+                        const uint64_t dbh = desc_sw128(st + kk * 32);
+                        const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
+                        if (P.exp_flags & 1) continue;
+                        mma_f16_ts(dcol, a_hi + ac, dbh, idesc, (kb | kk) != 0);
+                        mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
+                        mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
                     }
                     mma_commit(&empty[s]);
                 }
-                mma_commit(&tfull[ab]);
+                mma_commit(tfull);
                 if (tr && tc < 8) tr[16 + tc] = gtimer();
             }
             if (tr) tr[3] = gtimer();
         }
-    } else if (warp >= 2) {
-        // ---- epilogue warps 2..5: TMEM lane quarter q, lane = sample row
+    } else {
+        // ---- epilogue warps 2..17: lane quarter q, accumulator quarter qt
         const int q = warp & 3;
+        const int qt = (warp - 2) >> 2;
         const int row = q * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const float inv = 1.f / pow2_scale(2.f * P.scales[4] * P.scales[6]);
         const int64_t Mk = P.a.Mk;
-        constexpr int UU = CP > 16 ? CP / 16 : 1;
-        // drain accumulator buffer ab (tile column block nt) into acc
-        auto drain = [&](int ab, const float2 (&p0v)[XS], float2 (&acc)[CP]) {
-            const uint32_t taddr = lane_base + 256 + ab * 128;
-#pragma unroll
-            for (int chb = 0; chb < 4; chb += UU) {
-                if (P.exp_flags & 4) break;
-#pragma unroll
-                for (int h = 0; h < UU; ++h) {
-                    uint32_t r[32];
-                    tmem_ld32(taddr + (chb + h) * 32, r);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        const int j = (chb + h) * 16 + jj;  // complex column in tile
-                        const float2 gv = make_float2(__uint_as_float(r[2 * jj]),
-                                                      __uint_as_float(r[2 * jj + 1]));
-                        cfma(acc[j % CP], p0v[j / CP], gv);
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
-        };
         int tc = 0, seg = 0;
         for (int64_t us = u0; us < u1; ++seg) {
             const int64_t m = us / NT;
             const int64_t ue = min(u1, (m + 1) * NT);
             const int t = (int)(m / P.mt_per_frame);
             const bool last_seg = ue == u1;
-            // ---- this segment's N tiles: kd[k, c] += sum_x P0[k, x] G[k, (x, c)]
             const int64_t kloc = (int64_t)(m % P.mt_per_frame) * 128 + row;
             const bool valid = kloc < P.a.M;
             const float2 *p0row = P.p0p + ((int64_t)t * Mk + kloc) * P.a.nxp;
@@ -669,27 +634,23 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             float2 acc[CP];
 #pragma unroll
             for (int c = 0; c < CP; ++c) acc[c] = make_float2(0.f, 0.f);
-            float2 p0v[XS];
             for (int64_t u = us; u < ue; ++u, ++tc) {
                 const int nt = (int)(u - m * NT);
-                const int ab = tc & 1;
-                const uint32_t aph = (tc >> 1) & 1;
+                // this quarter's P0 values: complex columns [qt*32, qt*32+32)
+                float2 p0v[XQ];
+                const int xbase = (nt * 4 + qt) * XQ;
 #pragma unroll
-                for (int i = 0; i < XS; ++i)
-                    p0v[i] = valid ? p0row[nt * XS + i] : make_float2(0.f, 0.f);
+                for (int i = 0; i < XQ; ++i)
+                    p0v[i] = valid ? p0row[xbase + i] : make_float2(0.f, 0.f);
                 if (u + 1 == ue && !last_seg) {
-                    // the segment's last tile: load the next segment's A as
-                    // soon as the MMAs release the old one (the tile's
-                    // accumulator stays put in its TMEM buffer meanwhile),
-                    // so the tensor core waits only for the A load
+                    // the segment's last unit: load the next segment's A as
+                    // soon as the MMAs release the old one (the accumulator
+                    // stays put meanwhile)
                     mbar_wait(a_free, seg & 1);
                     tc_fence_after();
-                    load_a(ue / NT, lane_base, row);
-                    if (tr && threadIdx.x == 64 && seg < 1) tr[9] = gtimer();
+                    load_a(ue / NT, lane_base, row, qt);
                 }
-                if (u + 1 == ue && piece == 0 && npieces > 1) {
-                    // the other pieces of this tile finished long ago (their
-                    // CTAs started on it): fold them in before the last drain
+                if (u + 1 == ue && piece == 0 && npieces > 1 && qt == 0) {
                     for (int pc = 1; pc < npieces; ++pc) {
                         unsigned f = 0;
                         const unsigned *flag = P.tick + m * 4 + pc;
@@ -699,49 +660,81 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                         } while (f == 0u);
                     }
                 }
-                mbar_wait(&tfull[ab], aph);
+                mbar_wait(tfull, tc & 1);
                 tc_fence_after();
-                drain(ab, p0v, acc);
+                // this quarter (64 columns) in two 32-column reads; the
+                // accumulator is released right after the second read
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    uint32_t r[32];
+                    tmem_ld32(lane_base + 256 + qt * 64 + hh * 32, r);
+                    tmem_ld_wait();
+                    if (hh == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(tempty);
+                    }
+                    if (!(P.exp_flags & 4)) {
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {  // complex column in the quarter
+                            const int j = hh * 16 + jj;
+                            const float2 gv = make_float2(__uint_as_float(r[2 * jj]),
+                                                          __uint_as_float(r[2 * jj + 1]));
+                            cfma(acc[j % CP], p0v[j / CP], gv);
+                        }
+                    }
+                }
                 if (tr && threadIdx.x == 64 && tc < 8) tr[24 + tc] = gtimer();
             }
-            // ---- finish the segment.  A sample tile split across CTAs: the
-            // CTA holding its first units (piece 0; the tile is that CTA's
-            // last segment, so it is the last to get there) sums pieces
-            // 0, 1, ... in that order once their flags are up.
-            if (piece > 0) {
-                float2 *mine = P.kdp + ((int64_t)(piece - 1) * P.a.T * Mk + grow) * CP;
+            // ---- fold the four quarters (same rows) in quarter order, then
+            // finish the segment: piece 0 sums pieces 0, 1, ... in order
+#pragma unroll 1
+            for (int src = 1; src < 4; ++src) {
+                asm volatile("bar.sync 1, 512;" ::: "memory");
+                if (qt == src) {
 #pragma unroll
-                for (int c = 0; c < CP; ++c) mine[c] = acc[c];
-                __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (threadIdx.x == 64) {
-                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.tick + m * 4 + piece),
-                                 "r"(1u)
-                                 : "memory");
+                    for (int c = 0; c < CP; ++c) part_acc[row][c] = acc[c];
                 }
-            } else {
-                for (int pc = 1; pc < npieces; ++pc) {
-                    const float2 *src = P.kdp + ((int64_t)(pc - 1) * P.a.T * Mk + grow) * CP;
+                asm volatile("bar.sync 1, 512;" ::: "memory");
+                if (qt == 0) {
 #pragma unroll
-                    for (int c = 0; c < CP; ++c) acc[c] = cadd(acc[c], __ldcg(src + c));
+                    for (int c = 0; c < CP; ++c) acc[c] = cadd(acc[c], part_acc[row][c]);
                 }
-                if (npieces > 1) {
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (threadIdx.x < 64 + npieces - 1 && threadIdx.x >= 64)
-                        P.tick[m * 4 + 1 + (threadIdx.x - 64)] = 0u;  // re-arm
-                }
-                // max|kd| for the adjoint's operand scale (order-free)
-                float mx = 0.f;
+            }
+            if (qt == 0) {
+                if (piece > 0) {
+                    float2 *mine = P.kdp + ((int64_t)(piece - 1) * P.a.T * Mk + grow) * CP;
 #pragma unroll
-                for (int c = 0; c < CP; ++c)
-                    mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
+                    for (int c = 0; c < CP; ++c) mine[c] = acc[c];
+                    __threadfence();
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (threadIdx.x == 64) {
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;"
+                                     ::"l"(P.tick + m * 4 + piece), "r"(1u) : "memory");
+                    }
+                } else {
+                    for (int pc = 1; pc < npieces; ++pc) {
+                        const float2 *src = P.kdp + ((int64_t)(pc - 1) * P.a.T * Mk + grow) * CP;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(P.scales + 5), __float_as_uint(mx));
-                if (valid) {
-                    float2 *out = P.kdi + grow * CP;
+                        for (int c = 0; c < CP; ++c) acc[c] = cadd(acc[c], __ldcg(src + c));
+                    }
+                    if (npieces > 1) {
+                        asm volatile("bar.sync 2, 128;" ::: "memory");
+                        if (threadIdx.x < 64 + npieces - 1 && threadIdx.x >= 64)
+                            P.tick[m * 4 + 1 + (threadIdx.x - 64)] = 0u;  // re-arm
+                    }
+                    float mx = 0.f;
 #pragma unroll
-                    for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
+                    for (int c = 0; c < CP; ++c)
+                        mx = fmaxf(mx, fmaxf(fabsf(acc[c].x * inv), fabsf(acc[c].y * inv)));
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    if (lane == 0) atomicMax(reinterpret_cast<unsigned *>(P.scales + 5), __float_as_uint(mx));
+                    if (valid) {
+                        float2 *out = P.kdi + grow * CP;
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) out[c] = make_float2(acc[c].x * inv, acc[c].y * inv);
+                    }
                 }
             }
             us = ue;
@@ -1329,9 +1322,9 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup)
     tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS");
     if (tc.fwd_ts) {
-        const int NTt = tc.Nf / 128;
+        const int NTt = tc.Nf / 256;
         const int64_t units = mtiles * NTt;
-        tc.fts_smem = FTS_STAGES * FTS_KPS * 2 * FTS_B_TILE + 1024 + 256;
+        tc.fts_smem = FTS_STAGES * 2 * FTS_B_TILE + 1024 + 256;
         // CTAs = SMs (persistent); pieces of a sample tile split across CTAs
         // are limited to the 4 flag slots per tile
         auto max_pieces = [&](int64_t Gc) {
@@ -1440,8 +1433,8 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_fa_lo, tc.fa_lo, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
               tmap_f16_2d(&tc.tm_xb_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
-              tmap_f16_2d(&tc.tm_xb128_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
-              tmap_f16_2d(&tc.tm_xb128_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 128) &&
+              tmap_f16_2d(&tc.tm_xb256_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, 256) &&
+              tmap_f16_2d(&tc.tm_xb256_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 256) &&
               tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
@@ -1495,7 +1488,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         FwdTsParams P;
         P.a = a;
         P.mt_per_frame = tc.mt_f;
-        P.nt_tiles = tc.Nf / 128;
+        P.nt_tiles = tc.Nf / 256;
         P.units = (int64_t)tc.T * tc.mt_f * P.nt_tiles;
         P.fa_hi = reinterpret_cast<const uint4 *>(tc.fa_hi);
         P.fa_lo = reinterpret_cast<const uint4 *>(tc.fa_lo);
@@ -1510,16 +1503,23 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.probe = tc.probe;
         dim3 grid((unsigned)tc.fts_ctas);
         switch (tc.Cp) {
-            case 4: launch(k_tc_forward_ts<4>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
-            case 8: launch(k_tc_forward_ts<8>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
-            default: launch(k_tc_forward_ts<16>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb128_hi, tc.tm_xb128_lo, P); break;
+            case 4: launch(k_tc_forward_ts<4>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
+            case 8: launch(k_tc_forward_ts<8>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
+            default: launch(k_tc_forward_ts<16>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
         }
         if (user) {  // (T*M, C) copy for the caller
             int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
             launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, 1, tc.kdi, tc.kdi, user,
                    tc.red, tc.tick, tc.scales, gate);
         }
-        return cudaGetLastError() == cudaSuccess ? 0 : 3;
+        {
+        const cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) {
+            tc_last_error() = cudaGetErrorString(le);
+            return 3;
+        }
+    }
+    return 0;
     }
     const int G = tc.G;
     const bool direct = in_loop && !user && G == 1;
@@ -1547,7 +1547,14 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, G, tc.kdp, tc.kdi, user,
                                                                tc.red, tc.tick, tc.scales, gate);
     }
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    {
+        const cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) {
+            tc_last_error() = cudaGetErrorString(le);
+            return 3;
+        }
+    }
+    return 0;
 }
 
 // launches tc_forward makes (for the kernel-count bookkeeping)
@@ -1599,7 +1606,14 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
         default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
     }
     if (e != cudaSuccess) return 3;
-    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+    {
+        const cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) {
+            tc_last_error() = cudaGetErrorString(le);
+            return 3;
+        }
+    }
+    return 0;
 }
 
 }  // namespace csr
