@@ -298,3 +298,28 @@ def test_simulate_kspace_frames(cuda):
     for t in range(T):
         ref = O.forward_direct(img[t], sens, coords[t * M:(t + 1) * M])
         assert rel_err(ds.data[t * M:(t + 1) * M], ref) <= 1e-12
+
+
+def test_repeat_runs_bitwise_identical(cuda):
+    # deterministic device reductions: a race in the split-tile pieces, the
+    # grid barriers or the programmatic launches would show up here
+    from harness.configs import make_problem
+    prob = make_problem(0)
+    traj = P.Trajectory(prob.coords, prob.coords.shape[0], 1)
+    ds = P.KSpaceDataset(prob.data, traj)
+    params = P.ReconParams(**dict(prob.params, admm_max_iters=6))
+    ref, _ = P.admm_reconstruct(ds, prob.sens, params, compute_objectives=False)
+    for _ in range(3):
+        img, _ = P.admm_reconstruct(ds, prob.sens, params, compute_objectives=False)
+        assert np.array_equal(img, ref)
+    rng = np.random.default_rng(5)
+    for (nx, ny, C, M) in [(128, 128, 8, 16384), (40, 24, 3, 777), (64, 64, 16, 2000)]:
+        coords = rng.uniform(-0.5, 0.4999, size=(M, 2))
+        sens = random_complex(rng, (C, nx, ny))
+        op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens)
+        x = random_complex(rng, (nx, ny)).astype(np.complex64)
+        y = random_complex(rng, (M, C)).astype(np.complex64)
+        f0, a0 = op.forward(x), op.adjoint(y)
+        for _ in range(5):
+            assert np.array_equal(op.forward(x), f0)
+            assert np.array_equal(op.adjoint(y), a0)
