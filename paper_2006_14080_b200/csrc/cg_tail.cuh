@@ -289,6 +289,163 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
 }
 
 
+// One-barrier variant of the tail (default).  Phase A also accumulates
+// <r, Ad>, ||Ad||^2, ||r||^2 and max|Ad|, so after its single grid
+// reduction every block knows alpha = tau / <d, Ad> and, by expanding
+// ||r - alpha Ad||^2 = tau - 2 Re(alpha <r, Ad>) + |alpha|^2 ||Ad||^2 in
+// fp64, tau' and beta as well; x, r and d (with the next forward operand)
+// are then updated in one pass.  tau itself is re-measured directly
+// (||r||^2 in phase A) every iteration, so the expansion never compounds;
+// it differs from the directly summed ||r'||^2 of the reference only by the
+// fp32 rounding of r' (~1e-7 relative in beta).
+__global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
+    pdl_enter();
+    const Geom &g = A.g;
+    const AdmmBufs &b = A.b;
+    DevScalars *s = b.s;
+    if (!s->cg_active) return;  // uniform: every block reads the same flag
+    probe_enter(A.probe);
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const float dbound_old = A.scales[6];
+    const double atol2 = s->atol2;
+    const int cg_iter = s->cg_iter + 1, cg_max = s->cg_max, cur = s->cur;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    __shared__ unsigned gen0;
+    if (threadIdx.x == 0) gen0 = grid_gen(A.bar);
+    // ---- phase A: Ad; <d,Ad>, <r,Ad>, ||Ad||^2, ||r||^2; max|Ad|, max|r|
+    {
+        ThetaOf th{b.d, g, nullptr, nullptr};
+        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        float amax = 0.f, rmax = 0.f;
+        for (int64_t i = i0; i < g.n; i += stride) {
+            int t, xx, y;
+            unflat(g, i, t, xx, y);
+            const float2 f = coil_combine(A.ws, nullptr, A.S, g.T, 1, nxy, t, i - t * nxy);
+            const float2 l = theta_adj_at(th, g, t, xx, y);
+            const float2 a = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+            b.ad[i] = a;
+            const float2 d = b.d[i], r = b.r[i];
+            v[0] += (double)d.x * a.x + (double)d.y * a.y;
+            v[1] += (double)d.x * a.y - (double)d.y * a.x;
+            v[2] += (double)r.x * a.x + (double)r.y * a.y;
+            v[3] += (double)r.x * a.y - (double)r.y * a.x;
+            v[4] += (double)a.x * a.x + (double)a.y * a.y;
+            v[5] += (double)r.x * r.x + (double)r.y * r.y;
+            amax = fmaxf(amax, fmaxf(fabsf(a.x), fabsf(a.y)));
+            rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
+        }
+        __shared__ float shm[2][32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        }
+        if (lane == 0) {
+            shm[0][warp] = amax;
+            shm[1][warp] = rmax;
+        }
+        block_partials<6>(v, A.part);  // slots 0..5 (syncs the block)
+        if (warp == 0) {
+            const bool in = lane < (int)(blockDim.x >> 5);
+            float wa = in ? shm[0][lane] : 0.f, wr = in ? shm[1][lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                wa = fmaxf(wa, __shfl_xor_sync(0xffffffffu, wa, o));
+                wr = fmaxf(wr, __shfl_xor_sync(0xffffffffu, wr, o));
+            }
+            if (lane == 0) {
+                A.part[6 * (size_t)gridDim.x + blockIdx.x] = wa;
+                A.part[7 * (size_t)gridDim.x + blockIdx.x] = wr;
+            }
+        }
+    }
+    grid_barrier(A.bar, gen0 + 1);
+    double tot[6];
+    float amax_all, rmax_all;
+    {
+        __shared__ double res[6];
+        __shared__ float resm[2];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (warp == 0) {
+            double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            float ma = 0.f, mr = 0.f;
+            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) w[q] += __ldcg(A.part + (size_t)q * gridDim.x + bb);
+                ma = fmaxf(ma, (float)__ldcg(A.part + 6 * (size_t)gridDim.x + bb));
+                mr = fmaxf(mr, (float)__ldcg(A.part + 7 * (size_t)gridDim.x + bb));
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) w[q] = warp_sum(w[q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+                mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) res[q] = w[q];
+                resm[0] = ma;
+                resm[1] = mr;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 6; ++q) tot[q] = res[q];
+        amax_all = resm[0];
+        rmax_all = resm[1];
+    }
+    // fin_ad + fin_xr (solver.py:114-122), identically in every block
+    const double tau = tot[5];
+    const double den = tot[0] * tot[0] + tot[1] * tot[1];
+    const double al_re = tau * tot[0] / den, al_im = -tau * tot[1] / den;
+    const double tn = tau - 2.0 * (al_re * tot[2] - al_im * tot[3]) +
+                      (al_re * al_re + al_im * al_im) * tot[4];
+    const bool finite = isfinite(tn);
+    const double be_d = finite ? tn / tau : 0.0;
+    const bool go_on = finite && cg_iter < cg_max && tn > atol2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s->alpha_re = al_re;
+        s->alpha_im = al_im;
+        if (!finite) {
+            s->error = 1;
+            s->admm_active = 0;
+        } else {
+            s->beta_cg = be_d;
+        }
+        s->tau = tn;
+        s->cg_iter = cg_iter;
+        s->cg_active = go_on ? 1 : 0;
+    }
+    // ---- fused update: x += alpha d, r -= alpha Ad, d = r + beta d and
+    // the next forward operand (d only when CG goes on, as k_cg_d)
+    float2 *x = b.rho[cur ^ 1];
+    const float2 al = make_float2((float)al_re, (float)al_im);
+    const float2 nal = make_float2(-al.x, -al.y);
+    const float be = (float)be_d;
+    const float alabs = sqrtf(al.x * al.x + al.y * al.y);
+    const float dbound = rmax_all + 2.f * alabs * amax_all + fabsf(be) * dbound_old;
+    const float sg = pow2_scale(2.f * A.scales[4] * dbound);
+    if (go_on && blockIdx.x == 0 && threadIdx.x == 0) A.scales[5] = 0.f;
+    for (int64_t i = i0; i < g.n; i += stride) {
+        const float2 d = b.d[i];
+        x[i] = cadd(x[i], cmul(al, d));
+        const float2 r = cadd(b.r[i], cmul(nal, b.ad[i]));
+        b.r[i] = r;
+        if (go_on) {
+            const float2 nd = make_float2(r.x + be * d.x, r.y + be * d.y);
+            b.d[i] = nd;
+            int t, xx, y;
+            unflat(g, i, t, xx, y);
+            write_x_operand(A, t, xx, y, nxy, nd, sg);
+        }
+    }
+    if (go_on && blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
+    probe_exit(A.probe);
+}
+
 // ADMM iteration head (single rank, tensor-core operator): k_admm_mu +
 // k_admm_rhs + the first forward's k_tc_prep_x in one cooperative kernel
 // (solver.py:178-183, 99-108):

@@ -101,7 +101,7 @@ struct csr_plan {
     float2 *hprev = nullptr, *hnext = nullptr, *sfirst = nullptr, *slast = nullptr;
     double *loc = nullptr;
     double *mpart = nullptr;  // grid-max partials of the d producers
-    double *tail_part = nullptr;  // fused CG tail: [4][<= 1024 blocks] partials
+    double *tail_part = nullptr;  // fused CG head / tail: [8][<= 1024 blocks] partials
     int tail_blocks = 0;          // its cooperative grid (0: not computed yet)
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
@@ -334,7 +334,8 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU(cudaLaunchKernelEx(&cfg, head ? k_admm_head : k_cg_tail, A));
+    static const bool two_barriers = getenv("CSR_TAIL2") != nullptr;
+    CU(cudaLaunchKernelEx(&cfg, head ? k_admm_head : (two_barriers ? k_cg_tail : k_cg_tail1), A));
     LAUNCHED();
     return CSR_OK;
 }
@@ -555,7 +556,7 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         if ((rc = dalloc(p, &p->sfirst, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
         if ((rc = dalloc(p, &p->slast, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
     }
-    if ((rc = dalloc(p, &p->tail_part, (size_t)(4 * 1024), &p->ws_bytes))) return cleanup(rc);
+    if ((rc = dalloc(p, &p->tail_part, (size_t)(8 * 1024), &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->tickets, 16, &p->ws_bytes))) return cleanup(rc);
     if ((rc = dalloc(p, &p->sc, 1, &p->ws_bytes))) return cleanup(rc);
     if (cudaMemsetAsync(p->tickets, 0, 16 * sizeof(unsigned), st) != cudaSuccess)
