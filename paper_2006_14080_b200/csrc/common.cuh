@@ -40,6 +40,11 @@ enum ProbeSlot { PROBE_FWD = 0, PROBE_ADJ, PROBE_MU, PROBE_RHS, PROBE_PREP, PROB
 __device__ __forceinline__ void probe_enter(unsigned long long *pr) {
     if (pr && threadIdx.x == 0) atomicMax(&pr[0], ~(unsigned long long)gtimer());
 }
+// debug timeline (csr_debug_timeline): every probed launch appends
+// (slot, first start, last end) when enabled
+__device__ unsigned long long g_tl_ring[3 * 4096];
+__device__ unsigned g_tl_n;
+__device__ int g_tl_on;
 __device__ __forceinline__ void probe_exit(unsigned long long *pr) {
     if (!pr || threadIdx.x != 0) return;
     __threadfence();
@@ -50,6 +55,14 @@ __device__ __forceinline__ void probe_exit(unsigned long long *pr) {
         atomicAdd(&pr[2], t1 - t0);
         atomicAdd(&pr[3], 1ull);
         atomicExch(&pr[1], 0ull);
+        if (g_tl_on) {
+            const unsigned k = atomicAdd(&g_tl_n, 1u);
+            if (k < 4096) {
+                g_tl_ring[3 * k] = (unsigned long long)(size_t)pr;
+                g_tl_ring[3 * k + 1] = t0;
+                g_tl_ring[3 * k + 2] = t1;
+            }
+        }
     }
 }
 

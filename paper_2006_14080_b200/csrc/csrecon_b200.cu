@@ -938,6 +938,36 @@ int csr_plan_kernel_times(csr_plan *p, double *fwd_ms, double *adj_ms, int64_t *
     return CSR_OK;
 }
 
+// debug: enable (on = 1, clears) / read (on = 0) the per-launch timeline of
+// probed kernels: host gets n records (slot index, start ns, end ns)
+int csr_debug_timeline(csr_plan *p, int on, unsigned long long *host, int64_t cap) {
+    if (!p) return fail(CSR_ERR_ARG, "null plan");
+    CU(cudaSetDevice(p->dev));
+    CU(cudaDeviceSynchronize());
+    if (on) {
+        unsigned z = 0;
+        int one = 1;
+        CU(cudaMemcpyToSymbol(g_tl_n, &z, sizeof(z)));
+        CU(cudaMemcpyToSymbol(g_tl_on, &one, sizeof(one)));
+        return CSR_OK;
+    }
+    int zero = 0;
+    unsigned n = 0;
+    CU(cudaMemcpyToSymbol(g_tl_on, &zero, sizeof(zero)));
+    CU(cudaMemcpyFromSymbol(&n, g_tl_n, sizeof(n)));
+    n = std::min<unsigned>(n, 4096);
+    std::vector<unsigned long long> buf(3 * (size_t)n);
+    if (n) CU(cudaMemcpyFromSymbol(buf.data(), g_tl_ring, buf.size() * 8));
+    const uint64_t base = (uint64_t)(size_t)p->tc.probe;
+    const int64_t m = std::min<int64_t>(cap, n);
+    for (int64_t i = 0; i < m; ++i) {
+        host[3 * i] = base ? (buf[3 * i] - base) / 32 : 0;  // slot = offset / (4 u64)
+        host[3 * i + 1] = buf[3 * i + 1];
+        host[3 * i + 2] = buf[3 * i + 2];
+    }
+    return (int)m;
+}
+
 int csr_plan_set_timing(csr_plan *p, void *flush_buf, int64_t flush_bytes,
                         float *iter_ms) {
     if (!p) return fail(CSR_ERR_ARG, "null plan");
