@@ -352,7 +352,7 @@ inline bool use_cg_tail(const csr_plan *p) {
 }
 
 int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
-                           cudaStream_t st, int *nk) {
+                           cudaStream_t st, int *nk, bool snap) {
     const Geom g = p->g;
     const int eb = ew_blocks(g.n), ebD = ew_blocks(g.n * g.D);
     const int ebf = ew_blocks((int64_t)g.nx * g.ny);
@@ -423,7 +423,9 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     }
     launch(k_admm_post, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
     TRY(scalar_sync(p, b, FIN_POST, 4, 2, st, &k));
-    launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
+    if (snap) {  // per-iteration images only when the caller asked for them
+        launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
+    }
     *nk = k;
     return CSR_OK;
 }
@@ -775,7 +777,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     std::vector<double> key = {prm->lam, prm->lam_t, prm->beta,
                                (double)prm->cg_max_iters,
                                (double)(p->comm ? p->comm->nranks : 1),
-                               (double)(b.mr)};
+                               (double)(b.mr), (double)(snapshots != nullptr)};
     bool use_graph = true;
     if (!p->graph || p->graph_key != key) {
         if (p->graph) {
@@ -785,7 +787,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         cudaGraph_t graph = nullptr;
         CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         int nk = 0;
-        int rc = enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk);
+        int rc = enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk, snapshots != nullptr);
         cudaError_t ec = cudaStreamEndCapture(st, &graph);
         if (rc != CSR_OK) {
             if (graph) cudaGraphDestroy(graph);
@@ -828,7 +830,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
             CU(cudaGraphLaunch(p->graph, st));
         } else {
             int nk = 0;
-            TRY(enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk));
+            TRY(enqueue_admm_iteration(p, b, prm->cg_max_iters, st, &nk, snapshots != nullptr));
         }
         if (timed) CU(cudaEventRecord(p->iter_ev[2 * it + 1], st));
     }
