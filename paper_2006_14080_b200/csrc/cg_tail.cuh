@@ -448,13 +448,14 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
 
 // ADMM iteration head (single rank, tensor-core operator): k_admm_mu +
 // k_admm_rhs + the first forward's k_tc_prep_x in one cooperative kernel
-// (solver.py:178-183, 99-108):
-//   phase 1  mu+ = S(theta(rho) + eta)
+// with one grid barrier (solver.py:178-183, 99-108):
+//   phase 1  mu+ = S(theta(rho) + eta); max|mu - eta|, max|fhd| partials
 //   barrier  (the rhs stencil reads mu at neighbouring pixels)
 //   phase 2  rhs = fhd + (beta/2) Theta^H (mu - eta); x = 0; r = d = rhs;
-//            ||r||^2 and max|rhs| partials
-//   barrier  tau, CG activation (fin_rhs), sigma_x from the exact max
-//   phase 3  the forward operand of d
+//            the first forward operand of d, scaled from the bound
+//            max|rhs| <= max|fhd| + (beta/2) 2D max|mu - eta| (component-
+//            wise); ||r||^2 partials folded by the last block (ticket) in
+//            block order -> tau and the CG activation (fin_rhs)
 __global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
@@ -463,30 +464,81 @@ __global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
     if (!s->admm_active) return;  // uniform
     probe_enter(A.probe);
     const int64_t nxy = (int64_t)g.nx * g.ny;
-    const int cur = s->cur, cg_max = s->cg_max;
-    const double atol2 = s->atol2;
+    const int cur = s->cur;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     __shared__ unsigned gen0;
     if (threadIdx.x == 0) gen0 = grid_gen(A.bar);
-    // ---- phase 1: mu
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // ---- phase 1: mu, and the bounds of the rhs
     {
         const float2 *rho = b.rho[cur];
+        float mm = 0.f, fm = 0.f;
         for (int64_t i = i0; i < g.n * g.D; i += stride) {
             const int comp = (int)(i / g.n);
             int t, x, y;
             unflat(g, i - comp * g.n, t, x, y);
-            const float2 v = cadd(theta_at(rho, g, comp, t, x, y, nullptr), b.eta[i]);
-            b.mu[i] = soft1(v, comp == 2 ? b.t_t : b.t_s);
+            const float2 e = b.eta[i];
+            const float2 v = cadd(theta_at(rho, g, comp, t, x, y, nullptr), e);
+            const float2 m = soft1(v, comp == 2 ? b.t_t : b.t_s);
+            b.mu[i] = m;
+            mm = fmaxf(mm, fmaxf(fabsf(m.x - e.x), fabsf(m.y - e.y)));
+        }
+        for (int64_t i = i0; i < g.n; i += stride) {
+            const float2 f = b.fhd[i];
+            fm = fmaxf(fm, fmaxf(fabsf(f.x), fabsf(f.y)));
+        }
+        __shared__ float sh[2][32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+            fm = fmaxf(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+        }
+        if (lane == 0) {
+            sh[0][warp] = mm;
+            sh[1][warp] = fm;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const bool in = lane < (int)(blockDim.x >> 5);
+            float a = in ? sh[0][lane] : 0.f, c = in ? sh[1][lane] : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
+            }
+            if (lane == 0) {
+                A.part[blockIdx.x] = a;
+                A.part[gridDim.x + blockIdx.x] = c;
+            }
         }
     }
     grid_barrier(A.bar, gen0 + 1);
-    // ---- phase 2: rhs and the zero-start CG state
+    float bound;
+    {
+        __shared__ float rb;
+        if (warp == 0) {
+            float a = 0.f, c = 0.f;
+            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
+                a = fmaxf(a, (float)__ldcg(A.part + bb));
+                c = fmaxf(c, (float)__ldcg(A.part + gridDim.x + bb));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
+            }
+            if (lane == 0) rb = c + b.hb * 2.f * (float)g.D * a;
+        }
+        __syncthreads();
+        bound = rb;
+    }
+    const float sg = pow2_scale(2.f * A.scales[4] * bound);
+    // ---- phase 2: rhs, the zero-start CG state and the first operand
+    double v[1] = {0.0};
     {
         float2 *x = b.rho[cur ^ 1];
         MuMinusEta u{b.mu, b.eta, g, nullptr};
-        double v[1] = {0.0};
-        float dmax = 0.f;
         for (int64_t i = i0; i < g.n; i += stride) {
             int t, xx, y;
             unflat(g, i, t, xx, y);
@@ -497,71 +549,15 @@ __global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
             b.r[i] = rhs;
             b.d[i] = rhs;
             v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
-            dmax = fmaxf(dmax, fmaxf(fabsf(rhs.x), fabsf(rhs.y)));
-        }
-        __shared__ float shm[32];
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-        if (lane == 0) shm[warp] = dmax;
-        block_partials<1>(v, A.part);  // slot 0 (syncs the block)
-        if (warp == 0) {
-            float w = lane < (int)(blockDim.x >> 5) ? shm[lane] : 0.f;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
-            if (lane == 0) A.part[1 * (size_t)gridDim.x + blockIdx.x] = w;
+            write_x_operand(A, t, xx, y, nxy, rhs, sg);
         }
     }
-    grid_barrier(A.bar, gen0 + 2);
-    double tau;
-    float dmax_all;
-    {
-        __shared__ double r_tau;
-        __shared__ float r_max;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (warp == 0) {
-            double w = 0.0;
-            float m = 0.f;
-            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
-                w += __ldcg(A.part + bb);
-                m = fmaxf(m, (float)__ldcg(A.part + gridDim.x + bb));
-            }
-            w = warp_sum(w);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0) {
-                r_tau = w;
-                r_max = m;
-            }
-        }
-        __syncthreads();
-        tau = r_tau;
-        dmax_all = r_max;
-    }
-    // fin_rhs (solver.py:106-108), every block identically
-    const bool finite = isfinite(tau);
-    const bool go = finite && cg_max > 0 && tau > atol2;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        s->tau = tau;
-        s->cg_iter = 0;
-        if (!finite) {
-            s->error = 1;
-            s->cg_active = 0;
-            s->admm_active = 0;
-        } else {
-            s->cg_active = go ? 1 : 0;
-        }
-        A.scales[5] = 0.f;  // the forward's max|kd| (atomicMax)
-        A.scales[6] = dmax_all;
-    }
-    // ---- phase 3: the first forward's operand of d = rhs
-    if (go) {
-        const float sg = pow2_scale(2.f * A.scales[4] * dmax_all);
-        for (int64_t i = i0; i < g.n; i += stride) {
-            int t, xx, y;
-            unflat(g, i, t, xx, y);
-            write_x_operand(A, t, xx, y, nxy, b.d[i], sg);
-        }
+    // tau: the last block folds the per-block partials in block order
+    double tot[1];
+    if (grid_reduce<1>(v, A.part + 2 * (size_t)gridDim.x, A.bar + 2, tot) && threadIdx.x == 0) {
+        fin_rhs(s, tot[0]);  // tau, cg_iter = 0, CG activation / error
+        A.scales[5] = 0.f;   // the forward's max|kd| (atomicMax)
+        A.scales[6] = bound;
     }
     probe_exit(A.probe);
 }
