@@ -30,7 +30,7 @@ for i in range(n):
     r = (t[i] - t0) / 1e3
     d = (t[i, 0] - prev) / 1e3 if prev is not None else 0
     prev = t[i, 0]
-    if 100 <= i < 106:
+    if i < 6 or 20 <= i < 30 or i > n - 4:
         print(f"{i:3d} {r[0]:10.3f} {r[1]:10.3f} {r[2]:10.3f} {r[3]:10.3f}   {d:7.3f}")
 dm = np.diff(t[:n, 0]) / 1e3
 print("median mma step us", np.median(dm), "mean", dm.mean())
