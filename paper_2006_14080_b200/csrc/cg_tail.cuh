@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
     DevScalars *s = b.s;
     if (!s->cg_active) return;  // uniform: every block reads the same flag
     probe_enter(A.probe);
+    TAIL_STAMP(0);
     const int64_t nxy = (int64_t)g.nx * g.ny;
     const float dbound_old = A.scales[6];
     const double atol2 = s->atol2;
@@ -361,34 +362,38 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
             }
         }
     }
+    TAIL_STAMP(1);
     grid_barrier(A.bar, gen0 + 1);
+    TAIL_STAMP(2);
     double tot[6];
     float amax_all, rmax_all;
     {
         __shared__ double res[6];
         __shared__ float resm[2];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (warp == 0) {
-            double w[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            float ma = 0.f, mr = 0.f;
-            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
+        // warp q folds slot q; all of a lane's loads are issued at once
+        // (<= 8 * 32 blocks, the grid cap), then summed in block order
+        if (warp < 8) {
+            const int q = warp;
+            const double *src = A.part + (size_t)q * gridDim.x;
+            double xl[8];
 #pragma unroll
-                for (int q = 0; q < 6; ++q) w[q] += __ldcg(A.part + (size_t)q * gridDim.x + bb);
-                ma = fmaxf(ma, (float)__ldcg(A.part + 6 * (size_t)gridDim.x + bb));
-                mr = fmaxf(mr, (float)__ldcg(A.part + 7 * (size_t)gridDim.x + bb));
+            for (int u = 0; u < 8; ++u) {
+                const unsigned bb = lane + 32 * u;
+                xl[u] = bb < gridDim.x ? __ldcg(src + bb) : 0.0;
             }
+            double w = xl[0];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) w[q] = warp_sum(w[q]);
+            for (int u = 1; u < 8; ++u) w = q < 6 ? w + xl[u] : fmax(w, xl[u]);
+            if (q < 6) {
+                w = warp_sum(w);
+            } else {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
-                mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+                for (int o = 16; o > 0; o >>= 1) w = fmax(w, __shfl_xor_sync(0xffffffffu, w, o));
             }
             if (lane == 0) {
-#pragma unroll
-                for (int q = 0; q < 6; ++q) res[q] = w[q];
-                resm[0] = ma;
-                resm[1] = mr;
+                if (q < 6) res[q] = w;
+                else resm[q - 6] = (float)w;
             }
         }
         __syncthreads();
@@ -397,6 +402,7 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
         amax_all = resm[0];
         rmax_all = resm[1];
     }
+    TAIL_STAMP(3);
     // fin_ad + fin_xr (solver.py:114-122), identically in every block
     const double tau = tot[5];
     const double den = tot[0] * tot[0] + tot[1] * tot[1];
@@ -443,6 +449,7 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
         }
     }
     if (go_on && blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
+    TAIL_STAMP(7);
     probe_exit(A.probe);
 }
 
@@ -516,22 +523,23 @@ __global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
     grid_barrier(A.bar, gen0 + 1);
     float bound;
     {
-        __shared__ float rb;
-        if (warp == 0) {
-            float a = 0.f, c = 0.f;
-            for (unsigned bb = lane; bb < gridDim.x; bb += 32) {
-                a = fmaxf(a, (float)__ldcg(A.part + bb));
-                c = fmaxf(c, (float)__ldcg(A.part + gridDim.x + bb));
-            }
+        __shared__ float rm[2];
+        if (warp < 2) {  // warp q: max of slot q, all loads issued at once
+            float xl[8];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
-                c = fmaxf(c, __shfl_xor_sync(0xffffffffu, c, o));
+            for (int u = 0; u < 8; ++u) {
+                const unsigned bb = lane + 32 * u;
+                xl[u] = bb < gridDim.x ? (float)__ldcg(A.part + warp * gridDim.x + bb) : 0.f;
             }
-            if (lane == 0) rb = c + b.hb * 2.f * (float)g.D * a;
+            float a = xl[0];
+#pragma unroll
+            for (int u = 1; u < 8; ++u) a = fmaxf(a, xl[u]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+            if (lane == 0) rm[warp] = a;
         }
         __syncthreads();
-        bound = rb;
+        bound = rm[1] + b.hb * 2.f * (float)g.D * rm[0];
     }
     const float sg = pow2_scale(2.f * A.scales[4] * bound);
     // ---- phase 2: rhs, the zero-start CG state and the first operand
