@@ -112,6 +112,11 @@ __device__ __forceinline__ void all_totals(const double *part, double (&tot)[NV]
 // the forward's fp16 hi/lo operand for pixel (t, x, y) of image value v:
 // rows (x, c, Re/Im) doubled, sigma * s_c * v (k_tc_prep_x, valid entries only;
 // the zero padding is written once at plan build)
+// per-lane loads of the block-partial fold: grids of <= 32 * TAIL_FOLD blocks
+constexpr int TAIL_FOLD = 16;
+#ifndef XOP_COILS
+#define XOP_COILS 4
+#endif
 __device__ __forceinline__ void write_x_operand(const CgTailArgs &A, int t, int xx, int y,
                                                 int64_t nxy, float2 v, float sg) {
     const TcArgs &a = A.a;
@@ -119,13 +124,13 @@ __device__ __forceinline__ void write_x_operand(const CgTailArgs &A, int t, int 
     uint32_t *H = reinterpret_cast<uint32_t *>(A.xb_hi);
     uint32_t *L = reinterpret_cast<uint32_t *>(A.xb_lo);
     const int64_t p = (int64_t)xx * A.g.ny + y;
-    for (int c0 = 0; c0 < a.C; c0 += 8) {
-        float2 sv[8];
+    for (int c0 = 0; c0 < a.C; c0 += XOP_COILS) {
+        float2 sv[XOP_COILS];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < XOP_COILS; ++j)
             sv[j] = c0 + j < a.C ? A.sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < XOP_COILS; ++j) {
             const int c = c0 + j;
             if (c >= a.C) break;
             float2 w = cmul(sv[j], v);
@@ -144,7 +149,7 @@ __device__ __forceinline__ void write_x_operand(const CgTailArgs &A, int t, int 
     }
 }
 
-__global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
+__global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(256) k_cg_tail(CgTailArgs A) {
 // (||r||^2 in phase A) every iteration, so the expansion never compounds;
 // it differs from the directly summed ||r'||^2 of the reference only by the
 // fp32 rounding of r' (~1e-7 relative in beta).
-__global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
+__global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -372,19 +377,19 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
         __shared__ float resm[2];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         // warp q folds slot q; all of a lane's loads are issued at once
-        // (<= 8 * 32 blocks, the grid cap), then summed in block order
+        // (<= TAIL_FOLD * 32 blocks, the grid cap), then summed in block order
         if (warp < 8) {
             const int q = warp;
             const double *src = A.part + (size_t)q * gridDim.x;
-            double xl[8];
+            double xl[TAIL_FOLD];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < TAIL_FOLD; ++u) {
                 const unsigned bb = lane + 32 * u;
                 xl[u] = bb < gridDim.x ? __ldcg(src + bb) : 0.0;
             }
             double w = xl[0];
 #pragma unroll
-            for (int u = 1; u < 8; ++u) w = q < 6 ? w + xl[u] : fmax(w, xl[u]);
+            for (int u = 1; u < TAIL_FOLD; ++u) w = q < 6 ? w + xl[u] : fmax(w, xl[u]);
             if (q < 6) {
                 w = warp_sum(w);
             } else {
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(256) k_cg_tail1(CgTailArgs A) {
 //            max|rhs| <= max|fhd| + (beta/2) 2D max|mu - eta| (component-
 //            wise); ||r||^2 partials folded by the last block (ticket) in
 //            block order -> tau and the CG activation (fin_rhs)
-__global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
+__global__ void __launch_bounds__(256, 2) k_admm_head(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -525,15 +530,15 @@ __global__ void __launch_bounds__(256) k_admm_head(CgTailArgs A) {
     {
         __shared__ float rm[2];
         if (warp < 2) {  // warp q: max of slot q, all loads issued at once
-            float xl[8];
+            float xl[TAIL_FOLD];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < TAIL_FOLD; ++u) {
                 const unsigned bb = lane + 32 * u;
                 xl[u] = bb < gridDim.x ? (float)__ldcg(A.part + warp * gridDim.x + bb) : 0.f;
             }
             float a = xl[0];
 #pragma unroll
-            for (int u = 1; u < 8; ++u) a = fmaxf(a, xl[u]);
+            for (int u = 1; u < TAIL_FOLD; ++u) a = fmaxf(a, xl[u]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
             if (lane == 0) rm[warp] = a;

@@ -309,8 +309,8 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = 
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev));
         int64_t want = reduce_blocks(p->g.n * (p->C > 1 ? 2 : 1), TPB);
         if (const char *e = getenv("CSR_TAIL_BLOCKS")) want = atoi(e);
-        // <= 256 blocks: the one-barrier tail folds 8 partials per lane
-        p->tail_blocks = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)per_sm * sms, 256}));
+        // <= 32 * TAIL_FOLD blocks: the one-barrier tail folds TAIL_FOLD partials per lane
+        p->tail_blocks = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)per_sm * sms, (int64_t)32 * TAIL_FOLD}));
     }
     CgTailArgs A;
     A.g = p->g;

@@ -70,6 +70,30 @@ def test_operator_random_shapes_vs_direct_sum(cuda):
         assert rel_err(got, O.forward_direct(img, sens, coords)) <= OP_TOL
 
 
+@pytest.mark.parametrize("nx,ny,nc,m", [
+    (64, 64, 4, 4096),     # one half-empty adjoint y tile
+    (48, 192, 8, 2500),    # full tile + half tile (config 3's ny)
+    (40, 320, 3, 1800),    # two full tiles + a half tile, padded coils
+    (32, 200, 16, 1500),   # ny % 128 = 72, 16 coils
+    (96, 136, 5, 2048),    # ny % 128 = 8: a mostly empty last tile
+])
+def test_operator_tile_shapes_vs_oracle(cuda, nx, ny, nc, m):
+    # ragged adjoint y tiles (128 pixel rows, zero-padded factor rows) and
+    # forward K padding; both operators vs the f64 separable restatement
+    # (kernels.py:71-88)
+    rng = np.random.default_rng(nx * 1000 + ny)
+    coords = rng.uniform(-0.5, 0.4999, size=(m, 2))
+    sens = random_complex(rng, (nc, nx, ny))
+    img = random_complex(rng, (nx, ny))
+    y = random_complex(rng, (m, nc))
+    p0, p1 = O.build_factors(coords, nx, ny, "double")
+    op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens.astype(np.complex64))
+    ef = rel_err(op.forward(img.astype(np.complex64)), O.forward_sep(p0, p1, sens, img))
+    ea = rel_err(op.adjoint(y.astype(np.complex64)), O.adjoint_sep(p0, p1, sens, y))
+    assert ef <= OP_TOL, ef
+    assert ea <= OP_TOL, ea
+
+
 def test_adjointness(cuda):
     # test_operators.py:129-140 / criterion 2, in fp32
     rng = np.random.default_rng(44)
