@@ -30,6 +30,8 @@ struct CgTailArgs {
     TcArgs a;          // forward operand geometry
     const float2 *sens;
     __half *xb_hi, *xb_lo;
+    int write_x;       // write the next forward operand here (else k_tc_prep_x does,
+                       // from the bound left in scales[6])
     float *scales;     // [4] max|s|, [5] k-space max (reset), [6] bound on max|d|
     double *part;      // [3][grid] fp64 partials
     unsigned *bar;     // [2] grid barrier: arrivals, generation
@@ -106,47 +108,15 @@ __device__ __forceinline__ void all_totals(const double *part, double (&tot)[NV]
     for (int i = 0; i < NV; ++i) tot[i] = res[i];
 }
 
+// per-lane loads of the block-partial fold: grids of <= 32 * TAIL_FOLD blocks
+constexpr int TAIL_FOLD = 16;
+
 #define TAIL_STAMP(i) \
     if (A.stamps && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) \
     A.stamps[(blockIdx.x ? 16 : 0) + (i)] = gtimer()
-// the forward's fp16 hi/lo operand for pixel (t, x, y) of image value v:
-// rows (x, c, Re/Im) doubled, sigma * s_c * v (k_tc_prep_x, valid entries only;
-// the zero padding is written once at plan build)
-// per-lane loads of the block-partial fold: grids of <= 32 * TAIL_FOLD blocks
-constexpr int TAIL_FOLD = 16;
-#ifndef XOP_COILS
-#define XOP_COILS 4
-#endif
 __device__ __forceinline__ void write_x_operand(const CgTailArgs &A, int t, int xx, int y,
                                                 int64_t nxy, float2 v, float sg) {
-    const TcArgs &a = A.a;
-    const int hy = a.Kf / 2;
-    uint32_t *H = reinterpret_cast<uint32_t *>(A.xb_hi);
-    uint32_t *L = reinterpret_cast<uint32_t *>(A.xb_lo);
-    const int64_t p = (int64_t)xx * A.g.ny + y;
-    for (int c0 = 0; c0 < a.C; c0 += XOP_COILS) {
-        float2 sv[XOP_COILS];
-#pragma unroll
-        for (int j = 0; j < XOP_COILS; ++j)
-            sv[j] = c0 + j < a.C ? A.sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < XOP_COILS; ++j) {
-            const int c = c0 + j;
-            if (c >= a.C) break;
-            float2 w = cmul(sv[j], v);
-            w.x *= sg;
-            w.y *= sg;
-            __half rh, rl, ih, il;
-            split16(w.x, rh, rl);
-            split16(w.y, ih, il);
-            const int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)xx * a.Cp + c);
-            const int64_t e = row * hy + y, e1 = e + hy;
-            H[e] = pack2(rh, hneg(ih));
-            L[e] = pack2(rl, hneg(il));
-            H[e1] = pack2(ih, rh);
-            L[e1] = pack2(il, rl);
-        }
-    }
+    write_xop(A.a, A.sens, A.xb_hi, A.xb_lo, t, xx, y, nxy, v, sg);
 }
 
 __global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
@@ -286,7 +256,7 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
         b.d[i] = nd;
         int t, xx, y;
         unflat(g, i, t, xx, y);
-        write_x_operand(A, t, xx, y, nxy, nd, sg);
+        if (A.write_x) write_x_operand(A, t, xx, y, nxy, nd, sg);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
     TAIL_STAMP(7);
@@ -303,7 +273,11 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
 // (||r||^2 in phase A) every iteration, so the expansion never compounds;
 // it differs from the directly summed ||r'||^2 of the reference only by the
 // fp32 rounding of r' (~1e-7 relative in beta).
-__global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
+// XOP: this kernel also writes the next forward operand (small images,
+// latency-bound); without it (large images, bandwidth-bound) it runs at four
+// blocks per SM and k_tc_prep_x writes the operand
+template <bool XOP>
+__global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -324,14 +298,17 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
         ThetaOf th{b.d, g, nullptr, nullptr};
         double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         float amax = 0.f, rmax = 0.f;
-        for (int64_t i = i0; i < g.n; i += stride) {
+        auto load = [&](int64_t i, float2 &a, float2 &d, float2 &r) {
             int t, xx, y;
             unflat(g, i, t, xx, y);
             const float2 f = coil_combine(A.ws, nullptr, A.S, g.T, 1, nxy, t, i - t * nxy);
             const float2 l = theta_adj_at(th, g, t, xx, y);
-            const float2 a = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+            a = make_float2(f.x + b.hb * l.x, f.y + b.hb * l.y);
+            d = b.d[i];
+            r = b.r[i];
+        };
+        auto use = [&](int64_t i, float2 a, float2 d, float2 r) {
             b.ad[i] = a;
-            const float2 d = b.d[i], r = b.r[i];
             v[0] += (double)d.x * a.x + (double)d.y * a.y;
             v[1] += (double)d.x * a.y - (double)d.y * a.x;
             v[2] += (double)r.x * a.x + (double)r.y * a.y;
@@ -340,6 +317,17 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
             v[5] += (double)r.x * r.x + (double)r.y * r.y;
             amax = fmaxf(amax, fmaxf(fabsf(a.x), fabsf(a.y)));
             rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
+        };
+        // two grid-stride pixels per trip, all loads before the stores (more
+        // bytes in flight at large n); per-thread summation order unchanged
+        for (int64_t i = i0; i < g.n; i += 2 * stride) {
+            const int64_t j = i + stride;
+            const bool hj = j < g.n;
+            float2 a0, d0, r0, a1, d1, r1;
+            load(i, a0, d0, r0);
+            load(hj ? j : i, a1, d1, r1);
+            use(i, a0, d0, r0);
+            if (hj) use(j, a1, d1, r1);
         }
         __shared__ float shm[2][32];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -440,18 +428,26 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
     const float dbound = rmax_all + 2.f * alabs * amax_all + fabsf(be) * dbound_old;
     const float sg = pow2_scale(2.f * A.scales[4] * dbound);
     if (go_on && blockIdx.x == 0 && threadIdx.x == 0) A.scales[5] = 0.f;
-    for (int64_t i = i0; i < g.n; i += stride) {
-        const float2 d = b.d[i];
-        x[i] = cadd(x[i], cmul(al, d));
-        const float2 r = cadd(b.r[i], cmul(nal, b.ad[i]));
+    auto update = [&](int64_t i, float2 d, float2 xv, float2 rv, float2 adv) {
+        x[i] = cadd(xv, cmul(al, d));
+        const float2 r = cadd(rv, cmul(nal, adv));
         b.r[i] = r;
         if (go_on) {
             const float2 nd = make_float2(r.x + be * d.x, r.y + be * d.y);
             b.d[i] = nd;
             int t, xx, y;
             unflat(g, i, t, xx, y);
-            write_x_operand(A, t, xx, y, nxy, nd, sg);
+            if (XOP) write_x_operand(A, t, xx, y, nxy, nd, sg);
         }
+    };
+    for (int64_t i = i0; i < g.n; i += 2 * stride) {
+        const int64_t j = i + stride;
+        const bool hj = j < g.n;
+        const int64_t jj = hj ? j : i;
+        const float2 d0 = b.d[i], x0 = x[i], r0 = b.r[i], a0 = b.ad[i];
+        const float2 d1 = b.d[jj], x1 = x[jj], r1 = b.r[jj], a1 = b.ad[jj];
+        update(i, d0, x0, r0, a0);
+        if (hj) update(j, d1, x1, r1, a1);
     }
     if (go_on && blockIdx.x == 0 && threadIdx.x == 0) A.scales[6] = dbound;
     TAIL_STAMP(7);
@@ -468,7 +464,8 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail1(CgTailArgs A) {
 //            max|rhs| <= max|fhd| + (beta/2) 2D max|mu - eta| (component-
 //            wise); ||r||^2 partials folded by the last block (ticket) in
 //            block order -> tau and the CG activation (fin_rhs)
-__global__ void __launch_bounds__(256, 2) k_admm_head(CgTailArgs A) {
+template <bool XOP>
+__global__ void __launch_bounds__(256, XOP ? 2 : 4) k_admm_head(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -487,7 +484,7 @@ __global__ void __launch_bounds__(256, 2) k_admm_head(CgTailArgs A) {
         const float2 *rho = b.rho[cur];
         float mm = 0.f, fm = 0.f;
         for (int64_t i = i0; i < g.n * g.D; i += stride) {
-            const int comp = (int)(i / g.n);
+            const int comp = comp_of(g, i);
             int t, x, y;
             unflat(g, i - comp * g.n, t, x, y);
             const float2 e = b.eta[i];
@@ -562,7 +559,7 @@ __global__ void __launch_bounds__(256, 2) k_admm_head(CgTailArgs A) {
             b.r[i] = rhs;
             b.d[i] = rhs;
             v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
-            write_x_operand(A, t, xx, y, nxy, rhs, sg);
+            if (XOP) write_x_operand(A, t, xx, y, nxy, rhs, sg);
         }
     }
     // tau: the last block folds the per-block partials in block order

@@ -103,6 +103,11 @@ struct csr_plan {
     double *mpart = nullptr;  // grid-max partials of the d producers
     double *tail_part = nullptr;  // fused CG head / tail: [8][<= 1024 blocks] partials
     int tail_blocks = 0;          // its cooperative grid (0: not computed yet)
+    // the fused head / tail also write the next forward operand (C fp16 hi/lo
+    // row pairs per pixel: 48 of the tail's ~60 image-sized streams) unless
+    // the image is large enough for that stream to be bandwidth-bound: then
+    // the high-occupancy k_tc_prep_x writes it in its own launch
+    bool fuse_xop = true;
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
     int64_t flush_bytes = 0;
@@ -305,7 +310,10 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
 int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = false) {
     if (!p->tail_blocks) {
         int per_sm = 0, sms = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail, TPB, 0));
+        if (p->fuse_xop)
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail1<true>, TPB, 0));
+        else
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail1<false>, TPB, 0));
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev));
         int64_t want = reduce_blocks(p->g.n * (p->C > 1 ? 2 : 1), TPB);
         if (const char *e = getenv("CSR_TAIL_BLOCKS")) want = atoi(e);
@@ -321,6 +329,7 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = 
     A.sens = p->sens;
     A.xb_hi = p->tc.xb_hi;
     A.xb_lo = p->tc.xb_lo;
+    A.write_x = p->fuse_xop ? 1 : 0;
     A.scales = p->tc.scales;
     A.part = p->tail_part;
     A.bar = p->tickets + 8;
@@ -336,7 +345,11 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     static const bool two_barriers = getenv("CSR_TAIL2") != nullptr;
-    CU(cudaLaunchKernelEx(&cfg, head ? k_admm_head : (two_barriers ? k_cg_tail : k_cg_tail1), A));
+    void (*kern)(CgTailArgs);
+    if (head) kern = p->fuse_xop ? k_admm_head<true> : k_admm_head<false>;
+    else if (two_barriers) kern = k_cg_tail;
+    else kern = p->fuse_xop ? k_cg_tail1<true> : k_cg_tail1<false>;
+    CU(cudaLaunchKernelEx(&cfg, kern, A));
     LAUNCHED();
     return CSR_OK;
 }
@@ -396,7 +409,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     const int64_t nf = (int64_t)g.nx * g.ny;
     for (int it = 0; it < cg_max; ++it) {
         if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
-        const bool x_ready = tail;  // the head / previous tail wrote X
+        const bool x_ready = tail && p->fuse_xop;  // the head / previous tail wrote X
         TRY(run_forward(p, p->d, nullptr, st, gate, true, x_ready));
         k += p->tc.enabled ? tc_forward_launches(p->tc, true, false, x_ready) : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));
@@ -474,6 +487,13 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     p->C = desc->n_coils;
     p->M = desc->n_samples;
     p->g = make_geom(p->T, p->nx, p->ny);
+    {
+        // operand writes of >= CSR_XOP_SPLIT (default 2^22) coil-pixels go to
+        // their own kernel (measured crossover: tools/gpu/xop_ab.sh)
+        const char *e = getenv("CSR_XOP_SPLIT");
+        const int64_t lim = e ? atoll(e) : ((int64_t)1 << 22);
+        p->fuse_xop = p->g.n * p->C < lim;
+    }
     if (desc->flags & CSR_PLAN_FRAME_SHARD) {
         p->frame_mode = true;
         p->g.halo = 1;

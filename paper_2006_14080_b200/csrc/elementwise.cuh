@@ -116,10 +116,23 @@ struct ThetaOf {
 
 __device__ __forceinline__ void unflat(const Geom &g, int64_t p, int &t, int &x,
                                        int &y) {
+    if (p <= 0x7fffffff) {  // 32-bit division: the 64-bit one is a long call
+        const unsigned q = (unsigned)p, r = q / (unsigned)g.ny;
+        y = (int)(q - r * (unsigned)g.ny);
+        t = (int)(r / (unsigned)g.nx);
+        x = (int)(r - (unsigned)t * (unsigned)g.nx);
+        return;
+    }
     y = (int)(p % g.ny);
     int64_t r = p / g.ny;
     x = (int)(r % g.nx);
     t = (int)(r / g.nx);
+}
+
+// component index of an element of a (D, n) stack
+__device__ __forceinline__ int comp_of(const Geom &g, int64_t i) {
+    return (g.n <= 0x7fffffff && i <= 0x7fffffff) ? (int)((unsigned)i / (unsigned)g.n)
+                                                   : (int)(i / g.n);
 }
 
 __global__ void k_theta(Geom g, const float2 *__restrict__ img,
@@ -127,7 +140,7 @@ __global__ void k_theta(Geom g, const float2 *__restrict__ img,
     pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int comp = (int)(i / g.n);
+        int comp = comp_of(g, i);
         int t, x, y;
         unflat(g, i - comp * g.n, t, x, y);
         out[i] = theta_at(img, g, comp, t, x, y);
@@ -402,7 +415,7 @@ __global__ void k_admm_mu(Geom g, AdmmBufs b) {
     const int64_t nf = (int64_t)g.nx * g.ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int comp = (int)(i / g.n);
+        int comp = comp_of(g, i);
         int t, x, y;
         unflat(g, i - comp * g.n, t, x, y);
         float2 v = cadd(theta_at(rho, g, comp, t, x, y, b.hprev), b.eta[i]);
@@ -564,7 +577,7 @@ __global__ void k_admm_post(Geom g, AdmmBufs b) {
     double v[2] = {0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int comp = (int)(i / g.n);
+        int comp = comp_of(g, i);
         int64_t p = i - comp * g.n;
         int t, x, y;
         unflat(g, p, t, x, y);

@@ -263,8 +263,8 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         launch(k_tc_absmax_img, reduce_blocks(n, 256), 256, 0, st, img, n, tc.red, tc.tick,
                                                                tc.scales, gate);
     if (!x_ready) {  // else the fused CG tail already wrote X (cg_tail.cuh)
-        int64_t total = (int64_t)tc.T * tc.nxp * tc.Cp * tc.nyp;
-        int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+        // one thread per pixel, all coils
+        int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
         launch(k_tc_prep_x, nb, 256, 0, st, a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate,
                tc.probe ? tc.probe + 4 * PROBE_PREP : nullptr);
     }

@@ -187,7 +187,45 @@ __global__ void k_tc_absmax_img(const float2 *__restrict__ img, int64_t n, doubl
     if (grid_max(v, partials, ticket, m)) scales[6] = m;
 }
 
-// X' = split(sigma_x * s_c * img_t) laid out as doubled rows (x, c, part)
+// The forward's fp16 hi/lo operand entries of pixel (t, x, y) of image value
+// v: rows (x, c, Re/Im) doubled, X = sigma * s_c * v (valid x < nx, c < C,
+// y < ny only: the zero padding is written once at plan build).  Coil maps
+// are loaded four at a time (all in flight before the stores).
+constexpr int XOP_COILS = 4;
+__device__ __forceinline__ void write_xop(const TcArgs &a, const float2 *__restrict__ sens,
+                                          __half *xb_hi, __half *xb_lo, int t, int x, int y,
+                                          int64_t nxy, float2 v, float sg) {
+    const int hy = a.Kf / 2;  // complex y per row (nyp)
+    uint32_t *H = reinterpret_cast<uint32_t *>(xb_hi);
+    uint32_t *L = reinterpret_cast<uint32_t *>(xb_lo);
+    const int64_t p = (int64_t)x * a.ny + y;
+    for (int c0 = 0; c0 < a.C; c0 += XOP_COILS) {
+        float2 sv[XOP_COILS];
+#pragma unroll
+        for (int j = 0; j < XOP_COILS; ++j)
+            sv[j] = c0 + j < a.C ? sens[(int64_t)(c0 + j) * nxy + p] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < XOP_COILS; ++j) {
+            const int c = c0 + j;
+            if (c >= a.C) break;
+            float2 w = cmul(sv[j], v);
+            w.x *= sg;
+            w.y *= sg;
+            __half rh, rl, ih, il;
+            split16(w.x, rh, rl);
+            split16(w.y, ih, il);
+            const int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)x * a.Cp + c);
+            const int64_t e = row * hy + y, e1 = e + hy;
+            H[e] = pack2(rh, hneg(ih));
+            L[e] = pack2(rl, hneg(il));
+            H[e1] = pack2(ih, rh);
+            L[e1] = pack2(il, rl);
+        }
+    }
+}
+
+// X' = split(sigma_x * s_c * img_t) laid out as doubled rows (x, c, part):
+// one thread per pixel, all coils (valid entries only, see write_xop)
 __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
                             const float2 *__restrict__ sens, float *scales,
                             __half *hi, __half *lo, const int *gate,
@@ -198,34 +236,22 @@ __global__ void k_tc_prep_x(TcArgs a, const float2 *__restrict__ img,
     // exact power-of-two scale: |s_c * img| <= 2 max|s| max|img| (component-wise)
     const float sg = pow2_scale(2.f * scales[4] * scales[6]);
     if (blockIdx.x == 0 && threadIdx.x == 0) scales[5] = 0.f;  // k-space max (atomicMax)
-    const int hy = a.Kf / 2;  // complex y per row (nyp)
-    int64_t total = (int64_t)a.T * a.nxp * a.Cp * hy;
+    const int64_t nxy = (int64_t)a.nx * a.ny;
+    const int64_t total = (int64_t)a.T * nxy;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int y = (int)(i % hy);
-        int64_t r = i / hy;
-        int c = (int)(r % a.Cp);
-        r /= a.Cp;
-        int x = (int)(r % a.nxp);
-        int t = (int)(r / a.nxp);
-        float2 v = make_float2(0.f, 0.f);
-        if (x < a.nx && c < a.C && y < a.ny) {
-            int64_t p = (int64_t)x * a.ny + y;
-            v = cmul(sens[(int64_t)c * a.nx * a.ny + p], img[(int64_t)t * a.nx * a.ny + p]);
-            v.x *= sg;
-            v.y *= sg;
+        int t, x, y;
+        if (total <= 0x7fffffff) {
+            const unsigned q = (unsigned)i, r = q / (unsigned)a.ny;
+            y = (int)(q - r * (unsigned)a.ny);
+            t = (int)(r / (unsigned)a.nx);
+            x = (int)(r - (unsigned)t * (unsigned)a.nx);
+        } else {
+            y = (int)(i % a.ny);
+            x = (int)((i / a.ny) % a.nx);
+            t = (int)(i / nxy);
         }
-        __half rh, rl, ih, il;
-        split16(v.x, rh, rl);
-        split16(v.y, ih, il);
-        int64_t row = (int64_t)t * a.Nf + 2 * ((int64_t)x * a.Cp + c);
-        int64_t e = row * (a.Kf / 2) + y;               // uint32 (half2) index
-        int64_t e1 = e + a.Kf / 2;                      // next row (Im part)
-        uint32_t *H = reinterpret_cast<uint32_t *>(hi), *L = reinterpret_cast<uint32_t *>(lo);
-        H[e] = pack2(rh, hneg(ih));
-        L[e] = pack2(rl, hneg(il));
-        H[e1] = pack2(ih, rh);
-        L[e1] = pack2(il, rl);
+        write_xop(a, sens, hi, lo, t, x, y, nxy, img[i], sg);
     }
     probe_exit(probe);
 }
