@@ -68,10 +68,31 @@ typedef struct csr_plan_desc {
     int32_t flags;        /* CSR_PLAN_FRAME_SHARD: this plan holds a contiguous
                              block of the frames of a 2-D+t problem split across
                              ranks; temporal differences at the block edges use
-                             halo frames exchanged with the neighbour ranks */
+                             halo frames exchanged with the neighbour ranks.
+                             CSR_PLAN_ORDERED_SAMPLES: this plan holds a run of
+                             whole sample chunks of a static problem (see
+                             csr_sample_chunking) */
+    int64_t chunk_samples; /* CSR_PLAN_ORDERED_SAMPLES: the global chunk size */
+    int64_t total_samples; /* CSR_PLAN_ORDERED_SAMPLES: samples of the whole
+                              problem (all ranks) */
 } csr_plan_desc;
 
 #define CSR_PLAN_FRAME_SHARD 1
+#define CSR_PLAN_ORDERED_SAMPLES 2
+
+/* Order-stable sample sharding (the reference's default plan:
+ * make_shard_plan(n_samples, n_workers, chunk_size), sharding.py:76-113, with
+ * ChunkedDftOperator, operators.py:206-272, and ordered_chunk_sum,
+ * sharding.py:174-208).  The global chunk grid of a static problem: chunk
+ * k covers samples [k*chunk, min((k+1)*chunk, n_samples)).  A plan built with
+ * CSR_PLAN_ORDERED_SAMPLES over any contiguous run of whole chunks computes
+ * each of its samples' k-space values and each chunk's adjoint partial image
+ * bit-identically to a plan of the whole problem; with a comm attached the
+ * chunk partials of all ranks are gathered (NCCL all-gather) and folded in
+ * global chunk order, so every reduced image is bitwise independent of the
+ * number of ranks.  chunk is a multiple of 128 samples. */
+int csr_sample_chunking(int32_t nx, int32_t ny, int32_t n_coils, int64_t n_samples,
+                        int64_t *chunk_samples, int32_t *n_chunks);
 
 typedef struct csr_plan_info {
     int64_t factor_bytes;    /* resident encoding factors */
@@ -96,6 +117,12 @@ int csr_forward(csr_plan *plan, const void *image, void *kdata, void *stream);
 /* DftOperator.adjoint (operators.py:195-203 -> kernels.nudft_adjoint_sep,
  * kernels.py:81-88): kdata (T*M, C) -> image (T, nx, ny); no 1/N. */
 int csr_adjoint(csr_plan *plan, const void *kdata, void *image, void *stream);
+
+/* ChunkedDftOperator.adjoint (operators.py:254-265): the per-chunk partial
+ * images (n_chunks, nx, ny), unsummed, of an order-stable plan
+ * (CSR_PLAN_ORDERED_SAMPLES; n_chunks = csr_plan_info.split_k).  Other
+ * plans return their split-K partials. */
+int csr_adjoint_chunks(csr_plan *plan, const void *kdata, void *chunks, void *stream);
 
 /* normal_operator (solver.py:128-139) without the allreduce:
  * out = F^H F x + (beta/2) Theta^H Theta x. */

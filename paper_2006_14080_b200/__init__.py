@@ -12,10 +12,11 @@ from .acquisition import (ImageGrid, KSpaceDataset, SensitivityMaps, Trajectory,
                           simulate_kspace)
 from .errors import (CgDivergenceError, MemoryBudgetError, NativeError,
                      ShapeMismatchError, SpmdError)
-from .operators import (DEFAULT_MEMORY_BUDGET, DftFactors, DftOperator,
-                        build_factors)
-from .sharding import (CommStats, ShardPlan, coil_shard_plan, default_chunk_size,
-                       make_shard_plan)
+from .operators import (DEFAULT_MEMORY_BUDGET, ChunkedDftOperator, DftFactors,
+                        DftOperator, build_factors, sample_chunking)
+from .sharding import (CommStats, ShardPlan, allreduce_sum, coil_shard_plan,
+                       default_chunk_size, make_shard_plan, ordered_chunk_sum,
+                       sample_shard_plan)
 from .solver import (AdmmState, CgOutcome, ReconParams, RunReport,
                      admm_reconstruct, admm_step, adjoint_reconstruct, build_rhs,
                      cg_solve, normal_operator, objective, relative_change_sq,
@@ -35,9 +36,10 @@ def active_backend():
 __all__ = [
     "ImageGrid", "KSpaceDataset", "SensitivityMaps", "Trajectory", "simulate_kspace",
     "CgDivergenceError", "MemoryBudgetError", "NativeError", "ShapeMismatchError",
-    "SpmdError", "DEFAULT_MEMORY_BUDGET", "DftFactors", "DftOperator",
-    "build_factors", "CommStats", "ShardPlan", "coil_shard_plan",
-    "default_chunk_size", "make_shard_plan", "AdmmState", "CgOutcome",
+    "SpmdError", "DEFAULT_MEMORY_BUDGET", "ChunkedDftOperator", "DftFactors",
+    "DftOperator", "build_factors", "sample_chunking", "CommStats", "ShardPlan",
+    "allreduce_sum", "coil_shard_plan", "default_chunk_size", "make_shard_plan",
+    "ordered_chunk_sum", "sample_shard_plan", "AdmmState", "CgOutcome",
     "ReconParams", "RunReport", "admm_reconstruct", "admm_step",
     "adjoint_reconstruct", "build_rhs", "cg_solve", "normal_operator",
     "objective", "relative_change_sq", "should_continue", "axpy",

@@ -30,9 +30,11 @@ class PlanDesc(ctypes.Structure):
                 ("n_samples", ctypes.c_int64),
                 ("coords", ctypes.POINTER(ctypes.c_double)),
                 ("sens", ctypes.c_void_p), ("device", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("chunk_samples", ctypes.c_int64),
+                ("total_samples", ctypes.c_int64)]
 
 CSR_PLAN_FRAME_SHARD = 1
+CSR_PLAN_ORDERED_SAMPLES = 2
 
 
 class PlanInfo(ctypes.Structure):
@@ -68,6 +70,8 @@ SIGNATURES = {
     "csr_plan_get_factors": [_P, _I32, _P, _P, _P],
     "csr_forward": [_P, _P, _P, _P],
     "csr_adjoint": [_P, _P, _P, _P],
+    "csr_adjoint_chunks": [_P, _P, _P, _P],
+    "csr_sample_chunking": [_I32, _I32, _I32, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I32)],
     "csr_normal": [_P, _P, _P, _D, _P],
     "csr_theta": [_I32, _I32, _I32, _P, _P, _P],
     "csr_theta_adjoint": [_I32, _I32, _I32, _P, _P, _P],

@@ -108,6 +108,16 @@ struct csr_plan {
     // the image is large enough for that stream to be bandwidth-bound: then
     // the high-occupancy k_tc_prep_x writes it in its own launch
     bool fuse_xop = true;
+    // order-stable sample sharding (CSR_PLAN_ORDERED_SAMPLES): the plan's
+    // adjoint partials are whole global sample chunks; with a multi-rank comm
+    // they are all-gathered into gws ([nranks][S_max] chunk slots, rank-major
+    // = global chunk order, unused slots zero) and folded in that order
+    bool ordered = false;
+    int64_t chunk = 0, M_global = 0;
+    int n_chunks_total = 0, S_local = 1, S_max = 0;
+    int64_t ws_off = 0;     // this rank's first slot in ws (elements)
+    float2 *gws = nullptr;  // gathered chunk partials (multi-rank)
+    size_t gws_slots = 0;
     // benchmark timing (csr_plan_set_timing)
     void *flush_buf = nullptr;
     int64_t flush_bytes = 0;
@@ -191,10 +201,36 @@ int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
     return CSR_OK;
 }
 
+int nranks(const csr_plan *p) { return p->comm ? p->comm->nranks : 1; }
+
+// order-stable sample sharding across more than one rank
+bool ordered_multi(const csr_plan *p) { return p->ordered && nranks(p) > 1; }
+
+// image partial sums over ranks need an allreduce (coil sharding)
+bool coil_collective(const csr_plan *p) {
+    return !p->frame_mode && !p->ordered && nranks(p) > 1;
+}
+
 // split-K adjoint partials into p->ws; kd == nullptr reads the internal
 // buffer written by run_forward(..., nullptr)
 int run_adjoint_partials(csr_plan *p, const float2 *kd, cudaStream_t st,
                          const int *gate) {
+    if (p->tc.enabled && ordered_multi(p)) {
+        // one k-space scale for all ranks (max over ranks of max|kd|), the
+        // chunk partials into this rank's slots, then the all-gather
+        if (kd) {
+            tc_load_kd(p->tc, kd, st);
+            LAUNCHED();
+        }
+        NC(ncclAllReduce(p->tc.scales + 5, p->tc.scales + 5, 1, ncclFloat, ncclMax,
+                         p->comm->comm, st));
+        if (tc_adjoint(p->tc, nullptr, p->ws + p->ws_off, st, gate))
+            return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
+        g_launches.fetch_add(p->tc.adj_launches, std::memory_order_relaxed);
+        const size_t cnt = (size_t)p->S_max * p->g.n * 2;
+        NC(ncclAllGather(p->ws + p->ws_off, p->ws, cnt, ncclFloat, p->comm->comm, st));
+        return CSR_OK;
+    }
     if (p->tc.enabled) {
         if (tc_adjoint(p->tc, kd, p->ws, st, gate)) return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
         g_launches.fetch_add(p->tc.adj_launches + (kd ? 1 : 0), std::memory_order_relaxed);
@@ -227,8 +263,6 @@ int allreduce(csr_plan *p, float2 *buf, int64_t n_complex, cudaStream_t st) {
                      p->comm->comm, st));
     return CSR_OK;
 }
-
-int nranks(const csr_plan *p) { return p->comm ? p->comm->nranks : 1; }
 
 // frame-sharded plans finalise CG/ADMM scalars after an allreduce of the
 // per-rank sums (CSR_FORCE_MR exercises that path on one GPU)
@@ -362,7 +396,7 @@ int launch_admm_head(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
 
 inline bool use_cg_tail(const csr_plan *p) {
     static const bool off = getenv("CSR_NO_CG_TAIL") != nullptr;
-    return !off && p->tc.enabled && !p->frame_mode && !(p->comm && p->comm->nranks > 1);
+    return !off && p->tc.enabled && !p->frame_mode && !coil_collective(p);
 }
 
 int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
@@ -405,7 +439,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
         TRY(scalar_sync(p, b, FIN_RHS, 0, 1, st, &k));
     }
     const int *gate = &p->sc->cg_active;
-    const bool coil_multi = !fm && p->comm && p->comm->nranks > 1;
+    const bool coil_multi = coil_collective(p);
     const int64_t nf = (int64_t)g.nx * g.ny;
     for (int it = 0; it < cg_max; ++it) {
         if (fm) TRY(halo_exchange(p, p->d, p->d + (int64_t)(g.T - 1) * nf, st));
@@ -494,6 +528,22 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
         const int64_t lim = e ? atoll(e) : ((int64_t)1 << 22);
         p->fuse_xop = p->g.n * p->C < lim;
     }
+    if (desc->flags & CSR_PLAN_ORDERED_SAMPLES) {
+        if (desc->flags & CSR_PLAN_FRAME_SHARD) {
+            delete p;
+            return fail(CSR_ERR_ARG, "ordered sample sharding and frame sharding exclude each other");
+        }
+        if (p->T != 1 || desc->chunk_samples < 128 || desc->chunk_samples % 128 ||
+            desc->total_samples < p->M) {
+            delete p;
+            return fail(CSR_ERR_ARG, "ordered sample sharding needs T == 1, chunk_samples a "
+                                     "multiple of 128 and total_samples >= n_samples");
+        }
+        p->ordered = true;
+        p->chunk = desc->chunk_samples;
+        p->M_global = desc->total_samples;
+        p->n_chunks_total = (int)((p->M_global + p->chunk - 1) / p->chunk);
+    }
     if (desc->flags & CSR_PLAN_FRAME_SHARD) {
         p->frame_mode = true;
         p->g.halo = 1;
@@ -537,13 +587,16 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     // tensor-core operand build (returns tc.enabled=false for shapes it
     // does not tile; the SIMT kernels then handle the plan)
     if ((rc = tc_plan_build(p->tc, p->T, p->nx, p->ny, p->C, p->M, p->P0, p->P1, p->sens, st,
-                            &p->factor_bytes, &p->ws_bytes, p->allocs)))
+                            &p->factor_bytes, &p->ws_bytes, p->allocs, p->chunk, p->M_global)))
         return cleanup(fail(rc, "tensor-core plan: " + g_err));
+    if (p->ordered && !p->tc.enabled)
+        return cleanup(fail(CSR_ERR_ARG, "ordered sample sharding runs on the tensor-core "
+                                         "operator (<= 16 coils)"));
     ht.mark("tc plan");
     // workspace
     if ((rc = dalloc(p, &p->kd, (size_t)(rows * p->C), &p->ws_bytes))) return cleanup(rc);
     if (p->tc.enabled) {
-        p->S = p->tc.split;
+        p->S = p->S_local = p->tc.split;
         p->ws = p->tc.ws;
     } else {
         int tiles = ((p->nx + ST - 1) / ST) * ((p->ny + ST - 1) / ST);
@@ -614,7 +667,7 @@ int csr_plan_get_info(const csr_plan *p, csr_plan_info *info) {
     info->factor_bytes = p->factor_bytes;
     info->workspace_bytes = p->ws_bytes;
     info->gemm_path = p->tc.enabled ? 1 : 0;
-    info->split_k = p->S;
+    info->split_k = p->tc.enabled ? p->tc.split : p->S;
     return CSR_OK;
 }
 
@@ -735,7 +788,7 @@ int csr_adjoint_reconstruct(csr_plan *p, const void *kdata, void *image, void *s
     CU(cudaSetDevice(p->dev));
     cudaStream_t st = (cudaStream_t)stream;
     TRY(run_adjoint(p, (const float2 *)kdata, (float2 *)image, st));
-    TRY(allreduce(p, (float2 *)image, p->g.n, st));
+    if (coil_collective(p)) TRY(allreduce(p, (float2 *)image, p->g.n, st));
     return CSR_OK;
 }
 
@@ -772,7 +825,7 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
     CU(cudaEventRecord(p->ev[0], st));
     TRY(run_adjoint(p, (const float2 *)kdata, p->fhd, st));
     CU(cudaMemcpyAsync(p->rho[0], p->fhd, n * sizeof(float2), cudaMemcpyDeviceToDevice, st));
-    if (!p->frame_mode && p->comm && p->comm->nranks > 1) {
+    if (coil_collective(p)) {
         TRY(allreduce(p, p->rho[0], n, st));
         TRY(allreduce(p, p->fhd, n, st));
         ar_calls += 2;
@@ -884,7 +937,8 @@ int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
         for (int i = 0; i < hs.admm_iter; ++i) cg_total += hl[i].cg_iterations;
         if (hs.error) cg_total += hs.cg_iter;
         stats->allreduce_calls =
-            ar_calls + ((!p->frame_mode && p->comm && p->comm->nranks > 1) ? cg_total : 0);
+            ar_calls + (coil_collective(p) ? cg_total : 0) +
+            (ordered_multi(p) ? 2 + cg_total : 0);  // as ordered_chunk_sum calls
         stats->setup_ms = ms_setup;
         stats->solve_ms = ms_solve;
         if (timed) {
@@ -1045,6 +1099,50 @@ int csr_plan_set_comm(csr_plan *p, csr_comm *c) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
     }
+    if (p->ordered) {
+        CU(cudaSetDevice(p->dev));
+        if (c && c->nranks > 1) {
+            const int S_max = (p->n_chunks_total + c->nranks - 1) / c->nranks;
+            if (p->S_local > S_max)
+                return fail(CSR_ERR_ARG, "this rank holds more chunks than an even split allows "
+                                         "(use make_shard_plan with the chunk grid)");
+            const size_t slots = (size_t)c->nranks * S_max * p->g.n;
+            if (!p->gws || p->gws_slots != slots) {  // (a previous buffer stays in allocs)
+                TRY(dalloc(p, &p->gws, slots, &p->ws_bytes));
+                p->gws_slots = slots;
+            }
+            CU(cudaMemsetAsync(p->gws, 0, slots * sizeof(float2), p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            p->S_max = S_max;
+            p->ws = p->gws;
+            p->S = c->nranks * S_max;
+            p->ws_off = (int64_t)c->rank * S_max * p->g.n;
+        } else {
+            p->ws = p->tc.ws;
+            p->S = p->S_local;
+            p->ws_off = 0;
+        }
+    }
+    return CSR_OK;
+}
+
+int csr_sample_chunking(int32_t nx, int32_t ny, int32_t C, int64_t M, int64_t *chunk,
+                        int32_t *n_chunks) {
+    if (nx < 1 || ny < 1 || C < 1 || M < 1) return fail(CSR_ERR_SHAPE, "bad geometry");
+    if (!chunk || !n_chunks) return fail(CSR_ERR_ARG, "null argument");
+    int nc = 0;
+    tc_sample_chunking(nx, ny, C, M, *chunk, nc);
+    *n_chunks = nc;
+    return CSR_OK;
+}
+
+int csr_adjoint_chunks(csr_plan *p, const void *kdata, void *chunks, void *stream) {
+    if (!p || !kdata || !chunks) return fail(CSR_ERR_ARG, "null argument");
+    if (!p->tc.enabled) return fail(CSR_ERR_ARG, "chunk partials need the tensor-core operator");
+    CU(cudaSetDevice(p->dev));
+    if (tc_adjoint(p->tc, (const float2 *)kdata, (float2 *)chunks, (cudaStream_t)stream, nullptr))
+        return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
+    g_launches.fetch_add(p->tc.adj_launches + 1, std::memory_order_relaxed);
     return CSR_OK;
 }
 

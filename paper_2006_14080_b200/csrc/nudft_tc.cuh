@@ -78,10 +78,63 @@ inline void set_smem(F kernel, int bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+// Adjoint split-K cost model: waves of 148 CTAs x per-CTA time (blocks x
+// ~768 MMA cycles + chain drains + CTA setup/fill), bounded by the
+// partial-image memory; returns the number of k ranges S.
+inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes) {
+    int S = 1;
+    int64_t best_cost = INT64_MAX;
+    for (int c = 1; c <= std::min(kb_total, 1024); ++c) {
+        if (c > 1 && c * pix_bytes > ((int64_t)1 << 30)) break;
+        const int64_t kbps = (kb_total + c - 1) / c;
+        const int64_t nch = (kbps + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN;
+        const int64_t waves = (tiles * c + 147) / 148;
+        const int64_t cost = waves * (kbps * 768 + nch * 700 + 4000);
+        if (cost < best_cost) {
+            best_cost = cost;
+            S = c;
+        }
+    }
+    return S;
+}
+
+// Coil padding and adjoint tile count of a (T, nx, ny, C) plan.
+inline void tc_tiles(int T, int nx, int ny, int C, int &Cp, int64_t &tiles) {
+    Cp = 4;
+    while (Cp < C) Cp *= 2;
+    const int xs = 128 / Cp;
+    const int nxp = (nx + xs - 1) / xs * xs;
+    const int nyA = (ny + 127) / 128 * 128;
+    tiles = (int64_t)T * (nxp * Cp / 64) * (nyA / 128);
+}
+
+// Global sample-chunk grid of an order-stable sample-sharded problem
+// (T = 1): the k range of one adjoint split-K partial, a multiple of 128
+// samples so that every rank's chunk run starts on a forward sample tile.
+// The split is what a single plan of the whole problem would choose.
+inline void tc_sample_chunking(int nx, int ny, int C, int64_t M, int64_t &chunk,
+                               int &n_chunks) {
+    int Cp;
+    int64_t tiles;
+    tc_tiles(1, nx, ny, C, Cp, tiles);
+    const int kb_total = (int)((M + 127) / 128 * 128 / 32);
+    const int S = tc_split_model(tiles, kb_total, (int64_t)nx * ny * 8);
+    int kbps = (kb_total + S - 1) / S;
+    kbps = (kbps + 3) / 4 * 4;
+    chunk = (int64_t)kbps * 32;
+    n_chunks = (int)((M + chunk - 1) / chunk);
+}
+
+// chunk > 0: order-stable sample sharding (csr_plan_desc.chunk_samples):
+// the adjoint's k ranges are the global chunks (chunk / 32 blocks each) and
+// the forward is the tile-group form with the tile-group count of the
+// whole problem (M_global samples), so every sample's k-space value and
+// every chunk's partial image are the same bits whichever rank owns them.
 inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
                          const float2 *P0, const float2 *P1, const float2 *sens,
                          cudaStream_t st, int64_t *factor_bytes, int64_t *ws_bytes,
-                         std::vector<void *> &allocs) {
+                         std::vector<void *> &allocs, int64_t chunk = 0,
+                         int64_t M_global = 0) {
     tc.enabled = false;
     if (C > 16 || getenv("CSR_DISABLE_TC")) return 0;
     if (!get_encode()) return 0;
@@ -99,14 +152,18 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.nt = tc.Nf / TC_BN;
     tc.mt_f = (int)(tc.Mk / TC_BM);
     // forward groups: split the n-tiles so the grid covers the machine
-    const int64_t mtiles = (int64_t)T * tc.mt_f;
+    // (order-stable plans: the grouping of the whole problem)
+    const int64_t mtiles = chunk > 0 ? (int64_t)T * ((M_global + TC_BM - 1) / TC_BM)
+                                     : (int64_t)T * tc.mt_f;
     int G = 1;
     while (G < tc.nt && mtiles * G < 2 * 148 && tc.nt % (2 * G) == 0) G *= 2;
     tc.G = G;
     tc.nt_per_group = tc.nt / G;
     // A-stationary forward: 128-row B tiles; groups of tiles per CTA chosen
-    // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup)
-    tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS");
+    // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup).
+    // Its split of a sample tile into pieces depends on the grid, so the
+    // order-stable mode keeps the tile-group form.
+    tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS") && chunk == 0;
     if (tc.fwd_ts) {
         const int NTt = tc.Nf / 256;
         const int64_t units = mtiles * NTt;
@@ -140,24 +197,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // accumulation chains of <= TC_MAX_CHAIN blocks.  Pick S by a cost model
     // (waves of 148 CTAs x per-CTA time: blocks x ~768 MMA cycles + chain
     // drains + CTA setup/fill), bounded by the partial-image memory.
-    int S = 1;
-    {
-        const int64_t pix = (int64_t)T * nx * ny * 8;
-        int64_t best_cost = INT64_MAX;
-        for (int c = 1; c <= std::min(tc.kb_total, 1024); ++c) {
-            if (c > 1 && c * pix > ((int64_t)1 << 30)) break;
-            const int64_t kbps = (tc.kb_total + c - 1) / c;
-            const int64_t nch = (kbps + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN;
-            const int64_t waves = (tiles * c + 147) / 148;
-            const int64_t cost = waves * (kbps * 768 + nch * 700 + 4000);
-            if (cost < best_cost) {
-                best_cost = cost;
-                S = c;
-            }
-        }
-    }
+    int S = tc_split_model(tiles, tc.kb_total, (int64_t)T * nx * ny * 8);
     if (const char *e = getenv("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
+    if (chunk > 0) tc.kb_per_split = (int)(chunk / 32);
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
     tc.split = S;
     tc.raw_bytes = 32 * (64 / Cp) * 8 + 32 * Cp * 8;
@@ -350,15 +393,19 @@ inline int tc_forward_launches(const TcPlan &tc, bool in_loop, bool user, bool x
     return (in_loop ? 0 : 1) + (x_ready ? 1 : 2) + (direct ? 0 : 1);
 }
 
+// user (T*M, C) k-space -> tc.kdi, max|kd| -> scales[5]
+inline void tc_load_kd(TcPlan &tc, const float2 *user, cudaStream_t st) {
+    TcArgs a = tc_args(tc);
+    int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
+    launch(k_tc_load_kd, reduce_blocks(total, 256), 256, 0, st, a, user, tc.kdi, tc.red, tc.tick,
+                                                            tc.scales);
+}
+
 // kd already in tc.kdi (with sigma_d) when user == nullptr; else load it
 inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t st,
                       const int *gate) {
     TcArgs a = tc_args(tc);
-    if (user) {
-        int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-        launch(k_tc_load_kd, reduce_blocks(total, 256), 256, 0, st, a, user, tc.kdi, tc.red, tc.tick,
-                                                                tc.scales);
-    }
+    if (user) tc_load_kd(tc, user, st);
     AdjParams P;
     P.a = a;
     P.S = tc.split;

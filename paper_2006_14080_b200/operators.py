@@ -63,11 +63,15 @@ class DftOperator:
     @classmethod
     def build(cls, trajectory, grid, sens, mode="auto", precision="single",
               memory_budget=DEFAULT_MEMORY_BUDGET, n_frames=1, device=None,
-              frame_shard=False):
+              frame_shard=False, chunk_grid=None):
         """operators.py:141-164 (factor-cached, never materialized).
 
         frame_shard: the frames are one rank's block of a 2-D+t problem split
-        over ranks (temporal differences at the block edges use halo frames)."""
+        over ranks (temporal differences at the block edges use halo frames).
+        chunk_grid: (chunk_samples, total_samples) of an order-stable sample
+        split (``sample_chunking``); the coordinates are then a run of whole
+        chunks of that grid, and every k-space value and chunk partial comes
+        out bit-identical to a plan of the whole problem."""
         if mode not in MODES:
             raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
         validate_precision(precision)
@@ -88,12 +92,16 @@ class DftOperator:
                 np.ascontiguousarray(np.asarray(maps).astype(np.complex64))).to(dev)
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         m = coords.shape[0] // n_frames
+        flags = _native.CSR_PLAN_FRAME_SHARD if frame_shard else 0
+        chunk, total = (0, 0) if chunk_grid is None else (int(chunk_grid[0]), int(chunk_grid[1]))
+        if chunk_grid is not None:
+            flags |= _native.CSR_PLAN_ORDERED_SAMPLES
         desc = _native.PlanDesc(
             nx=grid.nx, ny=grid.ny, n_frames=n_frames, n_coils=tmaps.shape[0],
             n_samples=m,
             coords=coords.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-            sens=tmaps.data_ptr(), device=dev.index,
-            flags=_native.CSR_PLAN_FRAME_SHARD if frame_shard else 0)
+            sens=tmaps.data_ptr(), device=dev.index, flags=flags,
+            chunk_samples=chunk, total_samples=total)
         _dev.torch.cuda.current_stream(dev).synchronize()
         plan = ctypes.c_void_p()
         _native.call("csr_plan_create", ctypes.byref(desc), ctypes.byref(plan))
@@ -166,6 +174,17 @@ class DftOperator:
                      _dev.stream_ptr(self.device))
         return _dev.out_like(out, data)
 
+    def adjoint_chunks(self, data):
+        """Per-chunk adjoint partials (n_chunks, nx, ny), unsummed
+        (ChunkedDftOperator.adjoint, operators.py:254-265)."""
+        if self.n_frames != 1:
+            raise ValueError("chunk partials are defined for static (single-frame) plans")
+        y = _dev.as_c64(data, (self.n_samples, self.n_coils), "data", self.device)
+        out = _dev.empty_c64((self.info()["split_k"], self.nx, self.ny), self.device)
+        _native.call("csr_adjoint_chunks", self._plan, y.data_ptr(), out.data_ptr(),
+                     _dev.stream_ptr(self.device))
+        return _dev.out_like(out, data)
+
     def normal(self, x, beta=0.0):
         """F^H F x + (beta/2) Theta^H Theta x on this operator's shard."""
         t = _dev.as_c64(x, self.image_shape, "image", self.device)
@@ -173,6 +192,83 @@ class DftOperator:
         _native.call("csr_normal", self._plan, t.data_ptr(), out.data_ptr(),
                      float(beta), _dev.stream_ptr(self.device))
         return _dev.out_like(out, x)
+
+
+def sample_chunking(grid, n_coils, n_samples):
+    """(chunk_samples, n_chunks) of the global sample-chunk grid of a static
+    problem: the k ranges of the adjoint's per-chunk partials, a multiple of
+    128 samples (csr_sample_chunking).  Plays the role of the reference's
+    default_chunk_size (sharding.py:66-73) for order-stable plans."""
+    chunk, n = ctypes.c_int64(), ctypes.c_int32()
+    _native.call("csr_sample_chunking", grid.nx, grid.ny, int(n_coils), int(n_samples),
+                 ctypes.byref(chunk), ctypes.byref(n))
+    return chunk.value, n.value
+
+
+class ChunkedDftOperator:
+    """One worker's shard as a run of fixed global sample chunks
+    (operators.py:206-272).  The reference builds one DftOperator per chunk;
+    here one device plan covers the worker's contiguous chunk run and
+    computes each chunk's forward rows and adjoint partial exactly as a plan
+    of the whole problem would (``DftOperator.build(chunk_grid=...)``).
+    forward concatenates the chunks' rows; adjoint returns the per-chunk
+    partial images stacked (n_chunks, nx, ny), unsummed, for an
+    order-stable reduction keyed by chunk id (``ordered_chunk_sum``)."""
+
+    def __init__(self, op, chunk_ids):
+        self.op = op
+        self.chunk_ids = tuple(chunk_ids)
+        self.mode = op.mode
+        if len(self.chunk_ids) != op.info()["split_k"]:
+            raise ValueError(f"{len(self.chunk_ids)} chunk ids for a plan of "
+                             f"{op.info()['split_k']} chunks")
+
+    @classmethod
+    def build(cls, coords, grid, sens, chunk_ranges, chunk_ids, mode="auto",
+              precision="single", memory_budget=DEFAULT_MEMORY_BUDGET, chunk_size=None,
+              n_total=None, device=None):
+        """Chunks are absolute sample ranges of coords (consecutive).  The
+        chunk grid defaults to ``sample_chunking`` of the whole coords."""
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
+        coords = sample_coords(coords)
+        n_total = coords.shape[0] if n_total is None else n_total
+        maps = _maps_of(sens)
+        if chunk_size is None:
+            chunk_size, _ = sample_chunking(grid, maps.shape[0], n_total)
+        ranges = [tuple(r) for r in chunk_ranges]
+        if not ranges:
+            raise ValueError("chunked operator needs at least one chunk")
+        for (a, b), (c, _) in zip(ranges, ranges[1:]):
+            if b != c:
+                raise ValueError("chunk ranges must be consecutive")
+        for i, (a, b) in zip(chunk_ids, ranges):
+            if a != i * chunk_size or b != min((i + 1) * chunk_size, n_total):
+                raise ValueError(f"chunk {i} range {(a, b)} is not on the grid of "
+                                 f"{chunk_size}-sample chunks")
+        start, stop = ranges[0][0], ranges[-1][1]
+        op = DftOperator.build(coords[start:stop], grid, sens, mode=mode, precision=precision,
+                               memory_budget=memory_budget, device=device,
+                               chunk_grid=(chunk_size, n_total))
+        return cls(op, chunk_ids)
+
+    @property
+    def n_samples(self):
+        return self.op.n_samples
+
+    @property
+    def n_coils(self):
+        return self.op.n_coils
+
+    @property
+    def dtype(self):
+        return self.op.dtype
+
+    def forward(self, image):
+        return self.op.forward(image)
+
+    def adjoint(self, data):
+        return self.op.adjoint_chunks(data)
 
 
 def build_factors(trajectory, grid, precision="single", device=None):

@@ -7,7 +7,9 @@ B200 there is one process per GPU (``torch.distributed``) and the image
 partial sum is one NCCL allreduce issued inside the native CG loop, over
 NVLink/NVSwitch.  Coil sharding is used for static problems (F^H F is a sum
 over coils, like the sum over samples the reference shards) and frame
-sharding is planned for 2-D+t.
+sharding for 2-D+t.  The reference's order-stable sample
+split (``sample_shard_plan``; chunk partials all-gathered and folded in
+chunk order, bitwise independent of the worker count) is ``shard="sample"``.
 
 The sample-shard helpers (``make_shard_plan``, ``default_chunk_size``) are
 kept with the reference's semantics for API compatibility.
@@ -86,6 +88,70 @@ def make_shard_plan(n_total, n_workers, chunk_size=None):
         bounds.append((c0 * chunk_size, min(c1 * chunk_size, n_total)))
         c0 = c1
     return ShardPlan(n_total, tuple(bounds), chunk_size)
+
+
+def sample_shard_plan(grid, n_coils, n_samples, n_workers):
+    """Order-stable sample split of a static problem: contiguous runs of
+    whole chunks of the global chunk grid (``operators.sample_chunking``),
+    make_shard_plan(n_samples, n_workers, chunk_size) as the reference's
+    default plan (solver.py:296-297)."""
+    from .operators import sample_chunking
+    chunk, _ = sample_chunking(grid, n_coils, n_samples)
+    return make_shard_plan(n_samples, n_workers, chunk_size=chunk)
+
+
+def allreduce_sum(contributions, stats=None, phase="default"):
+    """Elementwise sum in ascending contributor order (sharding.py:151-170),
+    bitwise equal to adding left to right; host arrays."""
+    import numpy as np
+    if not contributions:
+        raise ValueError("allreduce needs at least one contribution")
+    first = np.asarray(contributions[0])
+    for c in contributions[1:]:
+        c = np.asarray(c)
+        if c.shape != first.shape:
+            raise ValueError(f"allreduce shape mismatch: {c.shape} vs {first.shape}")
+        if c.dtype != first.dtype:
+            raise ValueError(f"allreduce dtype mismatch: {c.dtype} vs {first.dtype}")
+    total = first.copy()
+    for c in contributions[1:]:
+        total += np.asarray(c)
+    if stats is not None:
+        stats.record(phase, total.size)
+    return total
+
+
+def ordered_chunk_sum(contributions, stats=None, phase="default"):
+    """Order-stable reduction (sharding.py:173-208): contributions are
+    (chunk_ids, stack) per worker; partials are folded by ascending global
+    chunk id, so the result does not depend on how chunks are distributed.
+    The device path does the same fold after an NCCL all-gather of the chunk
+    partials (csr_sample_chunking, CSR_PLAN_ORDERED_SAMPLES)."""
+    import numpy as np
+    if not contributions:
+        raise ValueError("allreduce needs at least one contribution")
+    pairs = []
+    for ids, stack in contributions:
+        if len(ids) != len(stack):
+            raise ValueError(f"worker sent {len(stack)} chunk partials for {len(ids)} ids")
+        pairs.extend(zip(ids, stack))
+    pairs.sort(key=lambda p: p[0])
+    ids = [i for i, _ in pairs]
+    if len(set(ids)) != len(ids):
+        raise ValueError("duplicate chunk ids across workers")
+    first = np.asarray(pairs[0][1])
+    for _, arr in pairs[1:]:
+        arr = np.asarray(arr)
+        if arr.shape != first.shape:
+            raise ValueError(f"allreduce shape mismatch: {arr.shape} vs {first.shape}")
+        if arr.dtype != first.dtype:
+            raise ValueError(f"allreduce dtype mismatch: {arr.dtype} vs {first.dtype}")
+    total = first.copy()
+    for _, arr in pairs[1:]:
+        total += np.asarray(arr)
+    if stats is not None:
+        stats.record(phase, total.size)
+    return total
 
 
 def coil_shard_plan(n_coils, n_workers):

@@ -24,7 +24,8 @@ from . import _dev, _native
 from .acquisition import ImageGrid
 from .errors import CgDivergenceError, ShapeMismatchError
 from .operators import DEFAULT_MEMORY_BUDGET, DftOperator
-from .sharding import CommStats, NcclComm, coil_shard_plan, dist_world, make_shard_plan
+from .sharding import (CommStats, NcclComm, coil_shard_plan, dist_world, make_shard_plan,
+                       sample_shard_plan)
 from .tensor import axpy, hermitian_dot, norm2_squared, validate_precision
 from .transform import soft_threshold, theta, theta_adjoint
 
@@ -265,25 +266,44 @@ class ShardSpec:
     sharding splits the coils (F^H F is a sum over coils, one image
     allreduce per CG iteration), ``frame`` sharding splits the frames of a
     2-D+t problem (F^H F is block diagonal; temporal differences exchange
-    one halo frame with each ring neighbour, CG scalars are allreduced)."""
+    one halo frame with each ring neighbour, CG scalars are allreduced),
+    ``sample`` sharding is the reference's order-stable split of a static
+    problem into runs of whole sample chunks (chunk partials all-gathered
+    and folded in chunk order: bitwise the same image for every world size,
+    sharding.py:173-208)."""
     mode: str
     frames: tuple
     coils: tuple
+    samples: tuple = None      # sample mode: this rank's [start, stop)
+    chunk_grid: tuple = None   # sample mode: (chunk_samples, total_samples)
+    chunk_ids: tuple = None    # sample mode: this rank's global chunk ids
 
 
-def plan_shard(n_frames, n_coils, rank, world, shard="auto"):
-    if shard not in ("auto", "coil", "frame"):
-        raise ValueError(f"shard must be auto, coil or frame, got {shard!r}")
+def plan_shard(n_frames, n_coils, rank, world, shard="auto", grid=None, n_samples=None):
+    if shard not in ("auto", "coil", "frame", "sample"):
+        raise ValueError(f"shard must be auto, coil, frame or sample, got {shard!r}")
     if shard == "auto":
         shard = "frame" if (n_frames > 1 and world > 1 and n_frames >= world) else "coil"
     if shard == "frame":
         return ShardSpec("frame", make_shard_plan(n_frames, world).bounds[rank],
                          (0, n_coils))
+    if shard == "sample":
+        if n_frames != 1:
+            raise ValueError("order-stable sample sharding is defined for static problems")
+        if grid is None or n_samples is None:
+            raise ValueError("sample sharding needs the image grid and the sample count")
+        plan = sample_shard_plan(grid, n_coils, n_samples, world)
+        ids, _ = plan.worker_chunks(rank)
+        return ShardSpec("sample", (0, 1), (0, n_coils), plan.bounds[rank],
+                         (plan.chunk_size, n_samples), ids)
     return ShardSpec("coil", (0, n_frames), coil_shard_plan(n_coils, world).bounds[rank])
 
 
 def shard_inputs(coords, data, maps, n_frames, spec):
     """This rank's (coords, data, maps) rows/columns for a ShardSpec."""
+    if spec.mode == "sample":
+        s0, s1 = spec.samples
+        return coords[s0:s1], np.asarray(data)[s0:s1], np.asarray(maps)
     m = coords.shape[0] // n_frames
     (f0, f1), (c0, c1) = spec.frames, spec.coils
     return (coords[f0 * m:f1 * m], np.asarray(data)[f0 * m:f1 * m, c0:c1],
@@ -301,13 +321,14 @@ class _Shard:
                              f"{world}: launch one process per GPU (torchrun)")
         T = _frames(dataset)
         self.rank, self.world, self.n_frames = rank, world, T
-        self.spec = plan_shard(T, maps.shape[0], rank, world, shard)
+        grid = ImageGrid(maps.shape[1], maps.shape[2])
         coords = np.asarray(dataset.trajectory.coords, dtype=np.float64)
+        self.spec = plan_shard(T, maps.shape[0], rank, world, shard, grid, coords.shape[0])
         lc, ld, lm = shard_inputs(coords, dataset.data, maps, T, self.spec)
         f0, f1 = self.spec.frames
-        grid = ImageGrid(maps.shape[1], maps.shape[2])
         self.op = DftOperator.build(lc, grid, lm, mode=op_mode, n_frames=f1 - f0,
-                                    device=device, frame_shard=self.spec.mode == "frame")
+                                    device=device, frame_shard=self.spec.mode == "frame",
+                                    chunk_grid=self.spec.chunk_grid)
         self.data = _dev.torch.from_numpy(
             np.ascontiguousarray(ld.astype(np.complex64))).to(self.op.device)
         self.comm = None
@@ -338,9 +359,14 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
     """Sharded ADMM reconstruction (solver.py:274-360). Returns (image, RunReport).
 
     n_workers must equal the torch.distributed world size (one process per
-    GPU; coils are split across ranks and the F^H F partials are summed by
-    one NCCL allreduce per CG iteration).  Objectives are evaluated after the
-    solve from per-iteration device snapshots and are not timed.
+    GPU).  shard="auto" splits coils across ranks (static; the F^H F partials
+    are summed by one NCCL allreduce per CG iteration) or frames (2-D+t).
+    shard="sample" is the reference's order-stable sample split: every rank
+    owns a run of whole global sample chunks, the chunk partials are
+    all-gathered and folded in chunk order, and the image is bitwise the same
+    for every n_workers (order_stable, solver.py:281-297).  Objectives are
+    evaluated after the solve from per-iteration device snapshots and are
+    not timed.
     """
     params = ReconParams() if params is None else params
     validate_precision(precision)
@@ -364,7 +390,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                 "cg_final_residual_sq": log[i].cg_final_residual_sq}
                for i in range(stats.n_iterations)]
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode == "coil":
+    if sh.world > 1 and sh.spec.mode in ("coil", "sample"):
         cs.record("setup", op.nx * op.ny * op.n_frames, calls=2)
         cs.record("solve", op.nx * op.ny * op.n_frames,
                   calls=stats.allreduce_calls - 2)
@@ -394,7 +420,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
         report.objective_initial = vals[0]
         for rec, val in zip(records, vals[1:]):
             rec["objective"] = val
-    if return_device and (sh.spec.mode == "coil" or sh.world == 1):
+    if return_device and (sh.spec.mode in ("coil", "sample") or sh.world == 1):
         return rho.reshape(sh.image_shape()), report
     return sh.gather(rho.cpu().numpy()), report
 
@@ -414,7 +440,7 @@ def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
                  _dev.stream_ptr(dev))
     _dev.torch.cuda.current_stream(dev).synchronize()
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode == "coil":
+    if sh.world > 1 and sh.spec.mode in ("coil", "sample"):
         cs.record("setup", op.nx * op.ny * op.n_frames)
     report = RunReport(
         method="adjoint", precision=precision, n_workers=n_workers, op_mode=op.mode,
@@ -423,6 +449,6 @@ def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
         timing={"setup_seconds": time.perf_counter() - t0,
                 "total_seconds": time.perf_counter() - t0},
         backend="csrecon_b200/" + op.info()["gemm_path"])
-    if return_device and (sh.spec.mode == "coil" or sh.world == 1):
+    if return_device and (sh.spec.mode in ("coil", "sample") or sh.world == 1):
         return img.reshape(sh.image_shape()), report
     return sh.gather(img.cpu().numpy()), report

@@ -144,6 +144,61 @@ def _coil_sharded_admm(rank, world, coords, sens, data, params, T):
     return spec, img
 
 
+def _chunked_partials(coords, sens, v, chunks, data=None):
+    """Per-chunk F^H F v (or F^H d) partials, each from its own samples only
+    (ChunkedDftOperator, operators.py:206-272)."""
+    out = []
+    for a, b in chunks:
+        p0, p1 = O.build_factors(coords[a:b], *sens.shape[1:])
+        d = data[a:b] if data is not None else O.forward_sep(p0, p1, sens, v)
+        out.append(O.adjoint_sep(p0, p1, sens, d))
+    return np.stack(out)
+
+
+def _ordered_admm(rank, world, coords, sens, data, params, chunk, gather):
+    """The device loop's order-stable sample decomposition
+    (CSR_PLAN_ORDERED_SAMPLES): each rank computes its chunks' partials, the
+    stacks are all-gathered and folded in global chunk order; everything
+    else is replicated."""
+    from paper_2006_14080_b200.sharding import make_shard_plan, ordered_chunk_sum
+    plan = make_shard_plan(coords.shape[0], world, chunk_size=chunk)
+    ids, ranges = plan.worker_chunks(rank)
+
+    def reduce(stack):
+        return ordered_chunk_sum(gather((ids, stack)))
+
+    fhd = reduce(_chunked_partials(coords, sens, None, ranges, data))
+    rho = fhd.copy()
+    mu = np.zeros((2,) + rho.shape, complex)
+    eta = mu.copy()
+    hb, t = params.beta / 2, params.lam / params.beta
+    for _ in range(params.admm_max_iters):
+        mu = O.soft_threshold(O.theta(rho) + eta, t)
+        rhs = fhd + hb * O.theta_adjoint(mu - eta)
+        x = np.zeros_like(rhs)
+        r = rhs.copy()
+        d = r.copy()
+        tau = np.vdot(r, r).real
+        for _ in range(params.cg_max_iters):
+            ad = reduce(_chunked_partials(coords, sens, d, ranges)) + \
+                hb * O.theta_adjoint(O.theta(d))
+            alpha = tau / np.vdot(d, ad)
+            x = x + alpha * d
+            r = r - alpha * ad
+            tn = np.vdot(r, r).real
+            d = r + (tn / tau) * d
+            tau = tn
+        eta = eta + (O.theta(x) - mu)
+        rho = x
+    return plan, rho
+
+
+def _gather_objects(obj):
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, obj)
+    return parts
+
+
 def _worker(rank, world, port, mode, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -152,6 +207,11 @@ def _worker(rank, world, port, mode, out_path):
         if mode == "uid":
             uid = broadcast_unique_id(rank, make_id=lambda: bytes(range(128)))
             res = {"uid": np.frombuffer(uid, np.uint8)}
+        elif mode == "sample":
+            coords, sens, data, params = _problem(1, m=150)
+            plan, img = _ordered_admm(rank, world, coords, sens, data, params, 32,
+                                      _gather_objects)
+            res = {"img": img, "bounds": np.array(plan.bounds[rank])}
         else:
             T = 4 if mode.startswith("frame") else (4 if mode == "coil_dyn" else 1)
             coords, sens, data, params = _problem(T)
@@ -195,6 +255,19 @@ def test_frame_sharded_admm_matches_unsharded(tmp_path):
     img = np.concatenate([r["img"] for r in res], axis=0)
     assert tuple(res[0]["frames"]) == (0, 2) and tuple(res[1]["frames"]) == (2, 4)
     assert np.linalg.norm(img - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_sample_sharded_admm_bitwise_independent_of_world(tmp_path):
+    # order-stable sample sharding (sharding.py:173-208): two ranks reproduce
+    # the one-rank result bit for bit
+    coords, sens, data, params = _problem(1, m=150)
+    _, ref = _ordered_admm(0, 1, coords, sens, data, params, 32, lambda o: [o])
+    res = _run("sample", tmp_path)
+    assert tuple(res[0]["bounds"]) == (0, 96) and tuple(res[1]["bounds"]) == (96, 150)
+    for r in res:
+        assert np.array_equal(r["img"], ref)
+    full, _ = O.admm(data, coords, sens, params, "double", 1)
+    assert np.linalg.norm(ref - full) <= 1e-10 * np.linalg.norm(full)
 
 
 def test_plan_shard_rules():

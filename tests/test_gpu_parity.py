@@ -347,3 +347,67 @@ def test_repeat_runs_bitwise_identical(cuda):
         for _ in range(5):
             assert np.array_equal(op.forward(x), f0)
             assert np.array_equal(op.adjoint(y), a0)
+
+
+# ---- order-stable sample sharding (sharding.py:173-208, operators.py:206-272)
+def _ordered_problem(nx, ny, nc, m, seed):
+    rng = np.random.default_rng(seed)
+    coords = rng.uniform(-0.5, 0.4999, size=(m, 2))
+    sens = random_complex(rng, (nc, nx, ny), np.complex64)
+    img = random_complex(rng, (nx, ny), np.complex64)
+    data = random_complex(rng, (m, nc), np.complex64)
+    return coords, sens, img, data
+
+
+@pytest.mark.parametrize("nx,ny,nc,m", [(128, 128, 8, 16384), (96, 80, 3, 10000)])
+def test_ordered_chunks_bitwise_for_every_split(cuda, nx, ny, nc, m):
+    # every sample's k-space value and every chunk's adjoint partial are the
+    # same bits whichever rank owns the chunk; the ordered fold of the
+    # ranks' stacks is the single-plan fold, bitwise
+    grid = P.ImageGrid(nx, ny)
+    coords, sens, img, data = _ordered_problem(nx, ny, nc, m, nx + m)
+    chunk, n_chunks = P.sample_chunking(grid, nc, m)
+    assert chunk % 128 == 0 and (n_chunks - 1) * chunk < m <= n_chunks * chunk
+    # the k-space operand scale is a power of two of max|data| on each plan
+    # (the multi-rank path allreduces it): give every chunk the same maximum
+    data[::chunk, 0] = 4.0
+    full = P.ChunkedDftOperator.build(coords, grid, sens, [(0, m)] if n_chunks == 1 else
+                                      [(i * chunk, min((i + 1) * chunk, m)) for i in range(n_chunks)],
+                                      range(n_chunks))
+    f_all = full.forward(img)
+    c_all = full.adjoint(data)
+    assert c_all.shape == (n_chunks, nx, ny)
+    ref = P.ordered_chunk_sum([(list(range(n_chunks)), c_all)])
+    for world in (2, 3, 4):
+        plan = P.make_shard_plan(m, world, chunk_size=chunk)
+        parts = []
+        for r in range(world):
+            ids, ranges = plan.worker_chunks(r)
+            op = P.ChunkedDftOperator.build(coords, grid, sens, ranges, ids)
+            s0, s1 = plan.bounds[r]
+            assert np.array_equal(op.forward(img), f_all[s0:s1]), (world, r)
+            stack = op.adjoint(data[s0:s1])
+            assert np.array_equal(stack, c_all[list(ids)]), (world, r)
+            parts.append((ids, stack))
+        assert np.array_equal(P.ordered_chunk_sum(parts[::-1]), ref)
+    # and the fold is the adjoint, to the operator tolerance
+    p0, p1 = O.build_factors(coords, nx, ny, "double")
+    assert rel_err(ref, O.adjoint_sep(p0, p1, sens.astype(complex), data.astype(complex))) <= OP_TOL
+
+
+def test_sample_shard_admm_matches_reference(cuda):
+    # shard="sample" on one rank: the order-stable plan (tile-group forward,
+    # chunked adjoint, fold in chunk order) through the native ADMM loop
+    g = golden("admm_small.npz")
+    lam, beta, rtol, na, atol, ncg = g["fixed_params"]
+    params = P.ReconParams(lam=lam, beta=beta, admm_rtol=rtol, admm_max_iters=int(na),
+                           cg_atol=atol, cg_max_iters=int(ncg))
+    ds = _dataset(g["coords"], g["data"])
+    img, rep = P.admm_reconstruct(ds, g["sens"], params, shard="sample",
+                                  compute_objectives=False)
+    assert rep.timing["shard"] == "sample"
+    assert rel_err(img, g["fixed_double_image"]) <= IMG_TOL
+    img2, _ = P.admm_reconstruct(ds, g["sens"], params, compute_objectives=False)
+    assert rel_err(img, img2) <= 1e-5
+    ad, _ = P.adjoint_reconstruct(ds, g["sens"], shard="sample")
+    assert rel_err(ad, g["adjoint_double"]) <= OP_TOL

@@ -50,6 +50,43 @@ def test_shard_plans():
         P.coil_shard_plan(4, 8)
 
 
+def test_sample_chunk_grid_and_ordered_sum():
+    # the global chunk grid of the order-stable split (csr_sample_chunking is
+    # host arithmetic: no GPU needed) and ordered_chunk_sum's semantics
+    # (sharding.py:173-208, test_sharding.py)
+    from paper_2006_14080_b200.solver import plan_shard
+    for nx, ny, nc, m in [(128, 128, 8, 16384), (256, 256, 16, 65536), (64, 64, 4, 4096),
+                          (96, 80, 3, 10000), (16, 12, 3, 240)]:
+        grid = P.ImageGrid(nx, ny)
+        chunk, n = P.sample_chunking(grid, nc, m)
+        assert chunk % 128 == 0 and (n - 1) * chunk < m <= n * chunk
+        for world in range(1, min(n, 8) + 1):
+            plan = P.sample_shard_plan(grid, nc, m, world)
+            assert plan.chunk_size == chunk and plan.bounds[-1][1] == m
+            assert all(a % chunk == 0 for a, _ in plan.bounds)
+            spec = plan_shard(1, nc, world - 1, world, "sample", grid, m)
+            assert spec.samples == plan.bounds[world - 1]
+            assert spec.chunk_grid == (chunk, m)
+            assert spec.chunk_ids == plan.worker_chunks(world - 1)[0]
+    with pytest.raises(ValueError):
+        plan_shard(4, 3, 0, 1, "sample", P.ImageGrid(8, 8), 100)
+    rng = np.random.default_rng(5)
+    parts = rng.standard_normal((7, 5, 4)).astype(np.float32)
+    ref = parts[0].copy()
+    for p in parts[1:]:
+        ref += p
+    for split in ([(0, 7)], [(0, 3), (3, 7)], [(0, 1), (1, 2), (2, 7)]):
+        contribs = [(list(range(a, b)), parts[a:b]) for a, b in split]
+        assert np.array_equal(P.ordered_chunk_sum(contribs[::-1]), ref)
+    with pytest.raises(ValueError):
+        P.ordered_chunk_sum([([0, 0], parts[:2])])
+    with pytest.raises(ValueError):
+        P.ordered_chunk_sum([([0], parts[:2])])
+    with pytest.raises(ValueError):
+        P.ordered_chunk_sum([])
+    assert np.array_equal(P.allreduce_sum([parts[0], parts[1]]), parts[0] + parts[1])
+
+
 def test_comm_stats_accounting():
     cs = P.CommStats()
     cs.record("setup", 100, calls=2)
