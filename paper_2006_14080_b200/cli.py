@@ -57,6 +57,9 @@ def _run_flags(p):
     p.add_argument("--op-mode", choices=("auto", "materialized", "separable"),
                    default="auto")
     p.add_argument("--memory-budget-gib", type=float, default=None)
+    p.add_argument("--shard", choices=("auto", "coil", "frame", "sample"), default="auto",
+                   help="work split across GPU workers; 'sample' is the reference's "
+                        "order-stable split (bitwise the same image for any --workers)")
 
 
 def build_parser():
@@ -129,11 +132,12 @@ def cmd_reconstruct(args):
     if args.method == "admm":
         image, report = admm_reconstruct(dataset, sens, _params(args),
                                          n_workers=args.workers, precision=precision,
-                                         op_mode=args.op_mode, memory_budget=budget)
+                                         op_mode=args.op_mode, memory_budget=budget,
+                                         shard=args.shard)
     else:
         image, report = adjoint_reconstruct(dataset, sens, n_workers=args.workers,
                                             precision=precision, op_mode=args.op_mode,
-                                            memory_budget=budget)
+                                            memory_budget=budget, shard=args.shard)
     rank = int(os.environ.get("RANK", "0"))
     report_path = args.report or f"{args.out}.report.json"
     if rank == 0:
@@ -159,7 +163,8 @@ def _best_time(args, workers):
         t0 = time.perf_counter()
         admm_reconstruct(dataset, sens, _params(args), n_workers=workers,
                          precision=PRECISION_FLAGS[args.precision], op_mode=args.op_mode,
-                         memory_budget=_memory_budget(args), compute_objectives=False)
+                         memory_budget=_memory_budget(args), compute_objectives=False,
+                         shard=args.shard)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
     return best
@@ -185,7 +190,7 @@ def _flags_for_worker(args):
            "--lambda", repr(args.lam), "--beta", repr(args.beta),
            "--admm-rtol", repr(args.admm_rtol), "--admm-iters", str(args.admm_iters),
            "--cg-atol", repr(args.cg_atol), "--cg-iters", str(args.cg_iters),
-           "--precision", args.precision, "--op-mode", args.op_mode]
+           "--precision", args.precision, "--op-mode", args.op_mode, "--shard", args.shard]
     if args.lam_t is not None:
         out += ["--lambda-t", repr(args.lam_t)]
     if args.memory_budget_gib is not None:
