@@ -73,6 +73,9 @@ constexpr int ADJ_MAX_RAW = 8;            // generator-input ring depth (max)
 // Barrier waits: the long ones (producers, epilogue) sleep on the barrier
 // (ADJ_SLEEP_SLOW), the latency-critical ones (MMA issuer, generators) spin
 // unless ADJ_SLEEP_FAST.
+#ifndef ADJ_ELECT
+#define ADJ_ELECT 1
+#endif
 #ifndef ADJ_SLEEP_SLOW
 #define ADJ_SLEEP_SLOW 1
 #endif
@@ -277,8 +280,10 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ---- MMA issuer
-        if (lane == 0) {
+        // ---- MMA issuer.  ADJ_ELECT: the whole warp runs the loop and one
+        // elected lane issues (warp-uniform descriptors: no per-MMA
+        // waterfall); else lane 0 alone.
+        if (ADJ_ELECT || lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, 128);
             constexpr uint32_t idesc256 = idesc_f16(128, 256);
             const uint32_t d_hi = tmem, d_lo = tmem + 128;
@@ -291,27 +296,32 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
                     const int s = i % ADJ_STAGES;
                     const uint32_t ph = (i / ADJ_STAGES) & 1;
                     wait_fast(&gen[s], ph);
-                    ADJ_TL(0, true);
+                    ADJ_TL(0, lane == 0);
                     wait_fast(&full[s], ph);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * ADJ_B_STAGE);
                     const uint32_t a_hi = tmem + 256 + 64 * s, a_lo = a_hi + 32;
-                    if (!(P.exp_flags & 2)) {
+                    const bool issue = ADJ_ELECT ? elect_one() : true;
+                    if (issue) {
+                        if (!(P.exp_flags & 2)) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            // B' = [hi_B ; lo_B] is one 256-row SW128 tile
-                            const uint64_t db = desc_sw128(st + kk * 32);
-                            const uint32_t acc = (i != i0) || (kk != 0);
-                            mma_f16_ts(d_hi, a_hi + 8 * kk, db, idesc256, acc);
-                            mma_f16_ts(d_lo, a_lo + 8 * kk, db, idesc, 1);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                // B' = [hi_B ; lo_B] is one 256-row SW128 tile
+                                const uint64_t db = desc_sw128(st + kk * 32);
+                                const uint32_t acc = (i != i0) || (kk != 0);
+                                mma_f16_ts(d_hi, a_hi + 8 * kk, db, idesc256, acc);
+                                mma_f16_ts(d_lo, a_lo + 8 * kk, db, idesc, 1);
+                            }
                         }
+                        // frees B stage s (TMA) and A stage s (generators)
+                        mma_commit(&empty[s]);
                     }
-                    // frees B stage s (TMA) and A stage s (generators)
-                    mma_commit(&empty[s]);
+                    if (ADJ_ELECT) __syncwarp();
                 }
-                mma_commit(acc_full);
+                if (ADJ_ELECT ? elect_one() : true) mma_commit(acc_full);
+                if (ADJ_ELECT) __syncwarp();
             }
-            if (tr) {
+            if (tr && lane == 0) {
                 tr[1] = gtimer();
                 tr[31] = clock64();
             }

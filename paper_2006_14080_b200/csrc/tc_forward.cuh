@@ -7,6 +7,18 @@
 
 namespace csr {
 
+// MMA issue from a whole warp with one elected lane (FWD_ELECT, default):
+// warp-uniform descriptors let ptxas issue UTCHMMA without the per-lane
+// waterfall loop it wraps around an MMA issued under lane == 0
+#ifndef FWD_ELECT
+#define FWD_ELECT 1
+#endif
+__device__ __forceinline__ bool fwd_one() { return FWD_ELECT ? sm100::elect_one() : true; }
+#ifndef FWD_SS_ELECT
+#define FWD_SS_ELECT 0
+#endif
+__device__ __forceinline__ bool fwd_ss_one() { return FWD_SS_ELECT ? sm100::elect_one() : true; }
+
 struct FwdParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
     TcArgs a;
@@ -83,7 +95,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // the whole warp runs the issue loop, one elected lane issues
+        // (warp-uniform descriptors: no per-MMA waterfall) when FWD_SS_ELECT;
+        // measured neutral-to-slower for this form (configs 2, 3), so off
+        if (FWD_SS_ELECT || lane == 0) {
             constexpr uint32_t idesc = idesc_f16(TC_BM, TC_BN);
             int it = 0, tc = 0;
             for (int nt = nt0; nt < nt1; ++nt, ++tc) {
@@ -100,18 +115,22 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                     const uint32_t st = smem_u32(smem + s * TC_FWD_OPS);
                     const uint32_t a_hi = st, a_lo = st + TC_A_TILE;
                     const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + TC_B_TILE;
+                    if (fwd_ss_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t o = kk * 32;
-                        const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
-                        const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
-                        mma_f16_fill(dcol, dah, dbh, idesc, (kb | kk) != 0);
-                        mma_f16_lastuse(dcol, dah, dbl, idesc, 1);
-                        mma_f16(dcol, dal, dbh, idesc, 1);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint32_t o = kk * 32;
+                            const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
+                            const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
+                            mma_f16_fill(dcol, dah, dbh, idesc, (kb | kk) != 0);
+                            mma_f16_lastuse(dcol, dah, dbl, idesc, 1);
+                            mma_f16(dcol, dal, dbh, idesc, 1);
+                        }
+                        mma_commit(&empty[s]);
                     }
-                    mma_commit(&empty[s]);
+                    if (FWD_SS_ELECT) __syncwarp();
                 }
-                mma_commit(&tfull[ab]);
+                if (fwd_ss_one()) mma_commit(&tfull[ab]);
+                if (FWD_SS_ELECT) __syncwarp();
             }
         }
     } else {
@@ -340,8 +359,9 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ---- MMA issuer
-        if (lane == 0) {
+        // ---- MMA issuer: the whole warp runs the loop, one elected lane
+        // issues (FWD_ELECT)
+        if (FWD_ELECT || lane == 0) {
             constexpr uint32_t idesc = idesc_f16(128, 256);
             const uint32_t a_hi = tmem, a_lo = tmem + 128, dcol = tmem + 256;
             int it = 0, tc = 0, seg = 0;
@@ -349,10 +369,11 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             for (int64_t u = u0; u < u1; ++u, ++tc) {
                 const int64_t m = u / NT;
                 if (m != m_prev) {  // new segment: wait for its A
-                    if (m_prev >= 0) mma_commit(a_free);  // old A is free after these MMAs
+                    if (m_prev >= 0 && fwd_one()) mma_commit(a_free);  // old A is free after these MMAs
+                    if (FWD_ELECT) __syncwarp();
                     mbar_wait(a_ready, seg & 1);
                     tc_fence_after();
-                    if (tr && seg < 2) tr[2 + seg * 4] = gtimer();
+                    if (tr && seg < 2 && lane == 0) tr[2 + seg * 4] = gtimer();
                     ++seg;
                     m_prev = m;
                 }
@@ -364,22 +385,26 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * STAGE);
+                    if (fwd_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t ac = kb * 32 + kk * 8;
-                        const uint64_t dbh = desc_sw128(st + kk * 32);
-                        const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
-                        if (P.exp_flags & 1) continue;
-                        mma_f16_ts(dcol, a_hi + ac, dbh, idesc, (kb | kk) != 0);
-                        mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
-                        mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint32_t ac = kb * 32 + kk * 8;
+                            const uint64_t dbh = desc_sw128(st + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
+                            if (P.exp_flags & 1) continue;
+                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, (kb | kk) != 0);
+                            mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
+                            mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
+                        }
+                        mma_commit(&empty[s]);
                     }
-                    mma_commit(&empty[s]);
+                    if (FWD_ELECT) __syncwarp();
                 }
-                mma_commit(tfull);
-                if (tr && tc < 8) tr[16 + tc] = gtimer();
+                if (fwd_one()) mma_commit(tfull);
+                if (FWD_ELECT) __syncwarp();
+                if (tr && tc < 8 && lane == 0) tr[16 + tc] = gtimer();
             }
-            if (tr) tr[3] = gtimer();
+            if (tr && lane == 0) tr[3] = gtimer();
         }
     } else {
         // ---- epilogue warps 2..17: lane quarter q, accumulator quarter qt
