@@ -411,3 +411,39 @@ def test_sample_shard_admm_matches_reference(cuda):
     assert rel_err(img, img2) <= 1e-5
     ad, _ = P.adjoint_reconstruct(ds, g["sens"], shard="sample")
     assert rel_err(ad, g["adjoint_double"]) <= OP_TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_full_size_config_operators(cuda, cfg):
+    # BASELINE configs 2-4 at full size (the CPU oracle cannot run them):
+    # size-independent properties of the tensor-core operator, and its
+    # forward against the f64 direct-sum encoder (simulate_kspace, itself
+    # pinned to the CPU oracle by test_simulate_kspace_f64_vs_direct_sum)
+    from harness.configs import make_problem
+
+    def enc(img, sens, coords):
+        return P.simulate_kspace(img, sens, coords).data
+
+    prob = make_problem(cfg, encoder=enc)
+    T = prob.n_frames
+    op = P.DftOperator.build(prob.coords, P.ImageGrid(prob.nx, prob.ny), prob.sens,
+                             n_frames=T)
+    truth = prob.truth.astype(np.complex64)
+    ref = P.simulate_kspace(prob.truth, prob.sens, prob.coords, n_frames=T).data
+    assert rel_err(op.forward(truth), ref) <= OP_TOL
+    rng = np.random.default_rng(cfg)
+    x1 = random_complex(rng, op.image_shape, np.complex64)
+    x2 = random_complex(rng, op.image_shape, np.complex64)
+    y = random_complex(rng, (op.n_samples, op.n_coils), np.complex64)
+    f1, f2 = op.forward(x1), op.forward(x2)
+    a, b = np.complex64(0.75 - 0.5j), np.complex64(-1.25 + 0.25j)
+    assert rel_err(op.forward(a * x1 + b * x2), a * f1 + b * f2) <= OP_TOL      # linearity
+    lhs = np.vdot(f1.astype(np.complex128), y.astype(np.complex128))
+    rhs = np.vdot(x1.astype(np.complex128), op.adjoint(y).astype(np.complex128))
+    # adjointness, relative to the Cauchy-Schwarz scale |F x| |y| (random x, y:
+    # <Fx, y> itself is a sum with heavy cancellation at 11M samples x coils)
+    scale = np.linalg.norm(f1.astype(np.complex128)) * np.linalg.norm(y.astype(np.complex128))
+    print(f"config {cfg}: |<Fx,y> - <x,F^H y>| / (|Fx||y|) = {abs(lhs - rhs) / scale:.2e}")
+    assert abs(lhs - rhs) <= 1e-6 * scale
+    ga, gb = op.adjoint(y), op.adjoint(2 * y)
+    assert np.array_equal(2 * ga, gb)                                          # exact scaling
