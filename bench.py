@@ -181,7 +181,7 @@ def run_reference(args, cfg, world, rank):
                     "d2h_bytes_per_step": 0}}
 
 
-def config_dict(cfg, world):
+def config_dict(cfg, world, shard=None):
     c = CONFIGS[cfg]
     m = c["spokes"] * c["readout"]
     return {"workload": f"BASELINE config {cfg}: ADMM-CG recon {c['nx']}x{c['ny']}"
@@ -190,7 +190,7 @@ def config_dict(cfg, world):
                         f"samples/frame, CG=5",
             "nx": c["nx"], "ny": c["ny"], "frames": c["n_frames"], "coils": c["n_coils"],
             "samples_per_frame": m, "cg_iters": 5, "lam": c["lam"], "beta": c["beta"],
-            "parallelism": f"coil-shard x{world}" if world > 1 else "1 GPU",
+            "parallelism": f"{shard or 'coil'}-shard x{world}" if world > 1 else "1 GPU",
             "l2": "flushed between timed iterations (256 MiB overwrite)"}
 
 
@@ -357,7 +357,7 @@ def run_ours(args, cfg, world, rank, local):
            "scaling": "strong", "vs_baseline": None, "dtype": "c64 (tcgen05 fp16x3-split GEMM, "
            "fp32 accumulate)" if op.info()["gemm_path"] == "tcgen05" else "c64 (fp32 SIMT)",
            "data": "synthetic (seeded BASELINE generators; no public dataset)",
-           "config": config_dict(cfg, world), "clocks": clk, "e2e": e2e,
+           "config": config_dict(cfg, world, sh.spec.mode), "clocks": clk, "e2e": e2e,
            "gpu_launches": int(kpi * args.steps), "roofline": roofline,
            "nudft_tflops": 5 * 2 * flops_launch / (1e3 * t_solve / args.steps) / 1e9,
            "backend": op.info()}

@@ -57,7 +57,7 @@ def _run_flags(p):
     p.add_argument("--op-mode", choices=("auto", "materialized", "separable"),
                    default="auto")
     p.add_argument("--memory-budget-gib", type=float, default=None)
-    p.add_argument("--shard", choices=("auto", "coil", "frame", "sample"), default="auto",
+    p.add_argument("--shard", choices=("auto", "coil", "frame", "sample", "split"), default="auto",
                    help="work split across GPU workers; 'sample' is the reference's "
                         "order-stable split (bitwise the same image for any --workers)")
 

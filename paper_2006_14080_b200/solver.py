@@ -270,7 +270,8 @@ class ShardSpec:
     ``sample`` sharding is the reference's order-stable split of a static
     problem into runs of whole sample chunks (chunk partials all-gathered
     and folded in chunk order: bitwise the same image for every world size,
-    sharding.py:173-208)."""
+    sharding.py:173-208), ``split`` the reference's plain sample split
+    (order_stable=False: one image allreduce per CG iteration, like coils)."""
     mode: str
     frames: tuple
     coils: tuple
@@ -279,11 +280,31 @@ class ShardSpec:
     chunk_ids: tuple = None    # sample mode: this rank's global chunk ids
 
 
+#: coils per rank below which coil sharding wastes tensor work (the
+#: operator pads a plan's coils to >= 4, tc_plan_build)
+MIN_COILS_PER_RANK = 4
+
+
 def plan_shard(n_frames, n_coils, rank, world, shard="auto", grid=None, n_samples=None):
-    if shard not in ("auto", "coil", "frame", "sample"):
-        raise ValueError(f"shard must be auto, coil, frame or sample, got {shard!r}")
+    """auto: frames for 2-D+t (world <= frames); coils for static problems
+    with >= 4 coils per rank; otherwise the plain sample split."""
+    if shard not in ("auto", "coil", "frame", "sample", "split"):
+        raise ValueError(f"shard must be auto, coil, frame, sample or split, got {shard!r}")
     if shard == "auto":
-        shard = "frame" if (n_frames > 1 and world > 1 and n_frames >= world) else "coil"
+        if n_frames > 1 and world > 1 and n_frames >= world:
+            shard = "frame"
+        elif (world > 1 and n_frames == 1 and n_coils < MIN_COILS_PER_RANK * world
+              and n_samples is not None and n_samples >= world):
+            shard = "split"
+        else:
+            shard = "coil"
+    if shard == "split":
+        if n_frames != 1:
+            raise ValueError("the sample split is defined for static problems")
+        if n_samples is None:
+            raise ValueError("sample sharding needs the sample count")
+        return ShardSpec("split", (0, 1), (0, n_coils),
+                         make_shard_plan(n_samples, world).bounds[rank])
     if shard == "frame":
         return ShardSpec("frame", make_shard_plan(n_frames, world).bounds[rank],
                          (0, n_coils))
@@ -301,7 +322,7 @@ def plan_shard(n_frames, n_coils, rank, world, shard="auto", grid=None, n_sample
 
 def shard_inputs(coords, data, maps, n_frames, spec):
     """This rank's (coords, data, maps) rows/columns for a ShardSpec."""
-    if spec.mode == "sample":
+    if spec.mode in ("sample", "split"):
         s0, s1 = spec.samples
         return coords[s0:s1], np.asarray(data)[s0:s1], np.asarray(maps)
     m = coords.shape[0] // n_frames
@@ -361,6 +382,8 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
     n_workers must equal the torch.distributed world size (one process per
     GPU).  shard="auto" splits coils across ranks (static; the F^H F partials
     are summed by one NCCL allreduce per CG iteration) or frames (2-D+t).
+    With few coils per rank (< 4: the operator pads coils to 4) the static
+    default is the plain sample split ("split", one image allreduce).
     shard="sample" is the reference's order-stable sample split: every rank
     owns a run of whole global sample chunks, the chunk partials are
     all-gathered and folded in chunk order, and the image is bitwise the same
@@ -390,7 +413,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                 "cg_final_residual_sq": log[i].cg_final_residual_sq}
                for i in range(stats.n_iterations)]
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode in ("coil", "sample"):
+    if sh.world > 1 and sh.spec.mode in ("coil", "sample", "split"):
         cs.record("setup", op.nx * op.ny * op.n_frames, calls=2)
         cs.record("solve", op.nx * op.ny * op.n_frames,
                   calls=stats.allreduce_calls - 2)
@@ -420,7 +443,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
         report.objective_initial = vals[0]
         for rec, val in zip(records, vals[1:]):
             rec["objective"] = val
-    if return_device and (sh.spec.mode in ("coil", "sample") or sh.world == 1):
+    if return_device and (sh.spec.mode in ("coil", "sample", "split") or sh.world == 1):
         return rho.reshape(sh.image_shape()), report
     return sh.gather(rho.cpu().numpy()), report
 
@@ -440,7 +463,7 @@ def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
                  _dev.stream_ptr(dev))
     _dev.torch.cuda.current_stream(dev).synchronize()
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode in ("coil", "sample"):
+    if sh.world > 1 and sh.spec.mode in ("coil", "sample", "split"):
         cs.record("setup", op.nx * op.ny * op.n_frames)
     report = RunReport(
         method="adjoint", precision=precision, n_workers=n_workers, op_mode=op.mode,
@@ -449,6 +472,6 @@ def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
         timing={"setup_seconds": time.perf_counter() - t0,
                 "total_seconds": time.perf_counter() - t0},
         backend="csrecon_b200/" + op.info()["gemm_path"])
-    if return_device and (sh.spec.mode in ("coil", "sample") or sh.world == 1):
+    if return_device and (sh.spec.mode in ("coil", "sample", "split") or sh.world == 1):
         return img.reshape(sh.image_shape()), report
     return sh.gather(img.cpu().numpy()), report

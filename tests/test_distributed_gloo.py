@@ -136,8 +136,8 @@ def _frame_sharded_admm(rank, world, coords, sens, data, params, T):
     return spec, rho
 
 
-def _coil_sharded_admm(rank, world, coords, sens, data, params, T):
-    spec = plan_shard(T, sens.shape[0], rank, world, "coil")
+def _coil_sharded_admm(rank, world, coords, sens, data, params, T, mode="coil"):
+    spec = plan_shard(T, sens.shape[0], rank, world, mode, n_samples=coords.shape[0])
     lc, ld, lm = shard_inputs(coords, data, sens, T, spec)
     op = O.Operator(lc, lm, T)
     img, recs = O.admm(ld, lc, lm, params, "double", T, allreduce=_allreduce, op=op)
@@ -215,8 +215,11 @@ def _worker(rank, world, port, mode, out_path):
         else:
             T = 4 if mode.startswith("frame") else (4 if mode == "coil_dyn" else 1)
             coords, sens, data, params = _problem(T)
-            fn = _frame_sharded_admm if mode.startswith("frame") else _coil_sharded_admm
-            spec, img = fn(rank, world, coords, sens, data, params, T)
+            if mode.startswith("frame"):
+                spec, img = _frame_sharded_admm(rank, world, coords, sens, data, params, T)
+            else:
+                spec, img = _coil_sharded_admm(rank, world, coords, sens, data, params, T,
+                                               "split" if mode == "split" else "coil")
             res = {"img": img, "frames": np.array(spec.frames), "coils": np.array(spec.coils)}
         np.savez(out_path.format(rank=rank), **res)
     finally:
@@ -235,13 +238,16 @@ def test_unique_id_broadcast(tmp_path):
         assert np.array_equal(r["uid"], np.arange(128, dtype=np.uint8))
 
 
-@pytest.mark.parametrize("mode", ["coil", "coil_dyn"])
+@pytest.mark.parametrize("mode", ["coil", "coil_dyn", "split"])
 def test_coil_sharded_admm_matches_unsharded(mode, tmp_path):
-    T = 1 if mode == "coil" else 4
+    T = 4 if mode == "coil_dyn" else 1
     coords, sens, data, params = _problem(T)
     ref, _ = O.admm(data, coords, sens, params, "double", T)
     res = _run(mode, tmp_path)
-    assert tuple(res[0]["coils"]) == (0, 2) and tuple(res[1]["coils"]) == (2, 4)
+    if mode == "split":  # every rank holds all coils and half the samples
+        assert tuple(res[0]["coils"]) == (0, 4) and tuple(res[1]["coils"]) == (0, 4)
+    else:
+        assert tuple(res[0]["coils"]) == (0, 2) and tuple(res[1]["coils"]) == (2, 4)
     for r in res:  # replicated image on every rank
         img = r["img"]
         assert np.linalg.norm(img - ref) <= 1e-10 * np.linalg.norm(ref)
@@ -275,6 +281,11 @@ def test_plan_shard_rules():
     assert plan_shard(64, 16, 3, 8).frames == (24, 32)
     assert plan_shard(1, 16, 3, 8).mode == "coil"
     assert plan_shard(1, 16, 3, 8).coils == (6, 8)
+    # fewer than 4 coils per rank (the operator pads coils to 4): sample split
+    assert plan_shard(1, 32, 3, 8, n_samples=16384).mode == "coil"
+    sp = plan_shard(1, 8, 3, 8, n_samples=16384)
+    assert sp.mode == "split" and sp.samples == (6144, 8192) and sp.coils == (0, 8)
+    assert plan_shard(1, 8, 1, 2, n_samples=16384).mode == "coil"
     assert plan_shard(4, 3, 0, 1, "frame").frames == (0, 4)
     with pytest.raises(ValueError):
         plan_shard(4, 3, 0, 1, "tiles")

@@ -409,6 +409,9 @@ def test_sample_shard_admm_matches_reference(cuda):
     assert rel_err(img, g["fixed_double_image"]) <= IMG_TOL
     img2, _ = P.admm_reconstruct(ds, g["sens"], params, compute_objectives=False)
     assert rel_err(img, img2) <= 1e-5
+    img3, rep3 = P.admm_reconstruct(ds, g["sens"], params, shard="split",
+                                    compute_objectives=False)
+    assert rep3.timing["shard"] == "split" and np.array_equal(img3, img2)
     ad, _ = P.adjoint_reconstruct(ds, g["sens"], shard="sample")
     assert rel_err(ad, g["adjoint_double"]) <= OP_TOL
 
