@@ -325,6 +325,29 @@ def run_ours(args, cfg, world, rank, local):
                 "step_breakdown_ms": {k: v["ms_per_launch"] * v["launches_per_step"]
                                       for k, v in breakdown.items()}}
 
+    # bandwidth-class loop kernels: algorithmic bytes per launch
+    # over the live per-launch time, against the measured HBM copy peak
+    V = 8.0 * op.nx * op.ny * op.n_frames          # one image-sized c64 vector
+    D = 3 if op.n_frames > 1 else 2
+    C, S = op.n_coils, op.info()["split_k"]
+    sens_b, xop_b = 8.0 * C * op.nx * op.ny, 16.0 * C * op.nx * op.ny * op.n_frames
+    fused = "operand_prep" not in breakdown      # the head / tail also write the operand
+    alg = {"cg_tail": (S + 11) * V + ((sens_b + xop_b) if fused else 0.0),
+           "admm_head_or_mu": (6 + 4 * D) * V + ((sens_b + xop_b) if fused else 0.0),
+           "admm_post": (2 + 3 * D) * V,
+           "operand_prep": V + sens_b + xop_b}
+    bw = {}
+    for name, nbytes in alg.items():
+        if name in breakdown and breakdown[name]["ms_per_launch"] > 0:
+            gbs = nbytes / (breakdown[name]["ms_per_launch"] * 1e-3) / 1e9
+            bw[name] = {"bytes_per_launch": nbytes, "ms_per_launch": breakdown[name]["ms_per_launch"],
+                        "achieved_gbs": gbs, "frac_of_hbm": gbs / pk["hbm_gbs"]}
+    roofline["bandwidth_kernels"] = {
+        "kernels": bw, "peak_gbs": pk["hbm_gbs"],
+        "note": ("image vectors of %.2f MB: L2-resident (126 MB L2), these kernels are "
+                 "latency-bound here; DESIGN.md §4 has config 4" % (V / 1e6))
+                if V * (S + 11) < 100e6 else "image vectors exceed L2"}
+
     # e2e through the public API with pinned host buffers
     e2e = None
     n_e2e = prob.params["admm_max_iters"]

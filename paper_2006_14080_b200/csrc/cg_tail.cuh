@@ -483,18 +483,26 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_admm_head(CgTailArgs A) {
     {
         const float2 *rho = b.rho[cur];
         float mm = 0.f, fm = 0.f;
-        for (int64_t i = i0; i < g.n * g.D; i += stride) {
-            const int comp = comp_of(g, i);
+        // pixel-major: every component of a pixel (and its fhd bound) with
+        // all loads ahead of the stores
+        for (int64_t p = i0; p < g.n; p += stride) {
             int t, x, y;
-            unflat(g, i - comp * g.n, t, x, y);
-            const float2 e = b.eta[i];
-            const float2 v = cadd(theta_at(rho, g, comp, t, x, y, nullptr), e);
-            const float2 m = soft1(v, comp == 2 ? b.t_t : b.t_s);
-            b.mu[i] = m;
-            mm = fmaxf(mm, fmaxf(fabsf(m.x - e.x), fabsf(m.y - e.y)));
-        }
-        for (int64_t i = i0; i < g.n; i += stride) {
-            const float2 f = b.fhd[i];
+            unflat(g, p, t, x, y);
+            float2 e[3], th[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c < g.D) {
+                    e[c] = b.eta[c * g.n + p];
+                    th[c] = theta_at(rho, g, c, t, x, y, nullptr);
+                }
+            const float2 f = b.fhd[p];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c < g.D) {
+                    const float2 m = soft1(cadd(th[c], e[c]), c == 2 ? b.t_t : b.t_s);
+                    b.mu[c * g.n + p] = m;
+                    mm = fmaxf(mm, fmaxf(fabsf(m.x - e[c].x), fabsf(m.y - e[c].y)));
+                }
             fm = fmaxf(fm, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
         __shared__ float sh[2][32];

@@ -419,7 +419,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
             if (!(skip & 8)) TRY(run_adjoint_partials(p, nullptr, st, nullptr));
             if (!(skip & 2)) TRY(launch_cg_tail(p, b, st));
         }
-        if (!(skip & 64)) launch(k_admm_post, ebD, TPB, 0, st, g, b);
+        if (!(skip & 64)) launch(k_admm_post, std::min(ebD, 148 * POST_BLOCKS_PER_SM), TPB, 0, st, g, b);
         if (!(skip & 128)) launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]);
         *nk = 0;
         return CSR_OK;
@@ -469,7 +469,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
         launch(k_stage_frames, ebf, TPB, 0, st, b, g, 1, p->sfirst, p->slast); LAUNCHED(); ++k;
         TRY(halo_exchange(p, p->sfirst, p->slast, st));
     }
-    launch(k_admm_post, ebD, TPB, 0, st, g, b); LAUNCHED(); ++k;
+    launch(k_admm_post, std::min(ebD, 148 * POST_BLOCKS_PER_SM), TPB, 0, st, g, b); LAUNCHED(); ++k;
     TRY(scalar_sync(p, b, FIN_POST, 4, 2, st, &k));
     if (snap) {  // per-iteration images only when the caller asked for them
         launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;

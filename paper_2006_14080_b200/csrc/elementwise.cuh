@@ -567,7 +567,9 @@ __global__ void k_cg_d(Geom g, AdmmBufs b) {
 // eta+ = eta + (theta(rho+) - mu+) (solver.py:186); alpha = ||rho+ -
 // rho||^2 / ||rho||^2 (solver.py:149-155,192); loop guard
 // should_continue (solver.py:158-160); iteration record (solver.py:318-323)
-__global__ void k_admm_post(Geom g, AdmmBufs b) {
+// launched with POST_BLOCKS_PER_SM blocks per SM: one wave of the grid-stride loop
+constexpr int POST_BLOCKS_PER_SM = 3;
+__global__ void __launch_bounds__(256, POST_BLOCKS_PER_SM) k_admm_post(Geom g, AdmmBufs b) {
     pdl_enter();
     DevScalars *s = b.s;
     if (!s->admm_active) return;
@@ -575,20 +577,46 @@ __global__ void k_admm_post(Geom g, AdmmBufs b) {
     const float2 *rho = b.rho[s->cur];
     const float2 *xn = b.rho[s->cur ^ 1];
     double v[2] = {0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n * g.D;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int comp = comp_of(g, i);
-        int64_t p = i - comp * g.n;
+    // pixel-major, all components of a pixel and two grid-stride pixels per
+    // trip with every load ahead of the stores (bytes in flight at large n);
+    // the launch grid is the (D, T, nx, ny) element grid of the earlier
+    // element-major form, so each thread sums the same pixels in the same
+    // order (bitwise-identical alpha)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    struct Px {
+        float2 e[3], th[3], m[3], a, o;
+    };
+    auto load = [&](int64_t p, Px &q) {
         int t, x, y;
         unflat(g, p, t, x, y);
-        float2 th = theta_at(xn, g, comp, t, x, y, b.hprev);
-        b.eta[i] = cadd(b.eta[i], csub(th, b.mu[i]));
-        if (comp == 0) {
-            float2 a = xn[p], o = rho[p];
-            float2 df = csub(a, o);
-            v[0] += (double)df.x * df.x + (double)df.y * df.y;
-            v[1] += (double)o.x * o.x + (double)o.y * o.y;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (c < g.D) {
+                q.e[c] = b.eta[c * g.n + p];
+                q.m[c] = b.mu[c * g.n + p];
+                q.th[c] = theta_at(xn, g, c, t, x, y, b.hprev);
+            }
         }
+        q.a = xn[p];
+        q.o = rho[p];
+    };
+    auto use = [&](int64_t p, const Px &q) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c < g.D) b.eta[c * g.n + p] = cadd(q.e[c], csub(q.th[c], q.m[c]));
+        const float2 df = csub(q.a, q.o);
+        v[0] += (double)df.x * df.x + (double)df.y * df.y;
+        v[1] += (double)q.o.x * q.o.x + (double)q.o.y * q.o.y;
+    };
+    for (int64_t p = i0; p < g.n; p += 2 * stride) {
+        const int64_t p1 = p + stride;
+        const bool h1 = p1 < g.n;
+        Px q0, q1;
+        load(p, q0);
+        load(h1 ? p1 : p, q1);
+        use(p, q0);
+        if (h1) use(p1, q1);
     }
     double tot[2];
     if (grid_reduce<2>(v, b.partials, b.tickets + 3, tot) && threadIdx.x == 0) {

@@ -307,7 +307,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
                                                                tc.scales, gate);
     if (!x_ready) {  // else the fused CG tail already wrote X (cg_tail.cuh)
         // one thread per pixel, all coils
-        int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * PREP_X_BLOCKS_PER_SM);
         launch(k_tc_prep_x, nb, 256, 0, st, a, img, tc.sens, tc.scales, tc.xb_hi, tc.xb_lo, gate,
                tc.probe ? tc.probe + 4 * PROBE_PREP : nullptr);
     }
@@ -338,7 +338,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         }
         if (user) {  // (T*M, C) copy for the caller
             int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-            launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, 1, tc.kdi, tc.kdi, user,
+            launch(k_tc_sum_kd, std::min(reduce_blocks(total, 256), 3 * 148), 256, 0, st, a, 1, tc.kdi, tc.kdi, user,
                    tc.red, tc.tick, tc.scales, gate);
         }
         {
@@ -373,7 +373,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
     }
     if (!direct) {
         int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;
-        launch(k_tc_sum_kd, reduce_blocks(total, 256), 256, 0, st, a, G, tc.kdp, tc.kdi, user,
+        launch(k_tc_sum_kd, std::min(reduce_blocks(total, 256), 3 * 148), 256, 0, st, a, G, tc.kdp, tc.kdi, user,
                                                                tc.red, tc.tick, tc.scales, gate);
     }
     {

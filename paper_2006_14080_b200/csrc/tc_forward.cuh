@@ -548,7 +548,8 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
 
 // kd = sum_g kdp[g]; writes the internal padded layout (and optionally a
 // user (T*M, C) layout); sigma_d from max|kd|
-__global__ void k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, float2 *kdi,
+// launched with <= 3 blocks per SM (one wave)
+__global__ void __launch_bounds__(256, 3) k_tc_sum_kd(TcArgs a, int G, const float2 *__restrict__ kdp, float2 *kdi,
                             float2 *user, double *partials, unsigned *ticket, float *scales,
                             const int *gate) {
     pdl_enter();
