@@ -577,13 +577,54 @@ __global__ void __launch_bounds__(256, POST_BLOCKS_PER_SM) k_admm_post(Geom g, A
     const float2 *rho = b.rho[s->cur];
     const float2 *xn = b.rho[s->cur ^ 1];
     double v[2] = {0.0, 0.0};
-    // pixel-major, all components of a pixel and two grid-stride pixels per
-    // trip with every load ahead of the stores (bytes in flight at large n);
-    // the launch grid is the (D, T, nx, ny) element grid of the earlier
-    // element-major form, so each thread sums the same pixels in the same
-    // order (bitwise-identical alpha)
+    // pixel-major, all components of a pixel with every load ahead of the
+    // stores (bytes in flight at large n).  Even ny: pixel pairs (y, y+1)
+    // with 16-byte loads / stores (the y-1 neighbour of the pair costs one
+    // extra 8-byte load); else two grid-stride pixels per trip.
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((g.ny & 1) == 0) {
+        const float4 *xn4 = reinterpret_cast<const float4 *>(xn);
+        const float4 *rho4 = reinterpret_cast<const float4 *>(rho);
+        const float4 *mu4 = reinterpret_cast<const float4 *>(b.mu);
+        float4 *eta4 = reinterpret_cast<float4 *>(b.eta);
+        const float4 *hp4 = reinterpret_cast<const float4 *>(b.hprev);
+        const int64_t n2 = g.n / 2, nxy = (int64_t)g.nx * g.ny;
+        for (int64_t j = i0; j < n2; j += stride) {
+            int t, x, y;
+            unflat(g, 2 * j, t, x, y);
+            float4 e[3], m[3], q[3];
+            const int64_t row = (int64_t)t * g.nx;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c < g.D) {
+                    e[c] = eta4[c * n2 + j];
+                    m[c] = mu4[c * n2 + j];
+                }
+            const float4 a = xn4[j], o = rho4[j];
+            // theta neighbours (theta_at): x-1 pair, y-1 single, t-1 pair
+            q[0] = xn4[((row + (x == 0 ? g.nx - 1 : x - 1)) * g.ny + y) >> 1];
+            const float2 qy = xn[(row + x) * g.ny + (y == 0 ? g.ny - 1 : y - 1)];
+            if (g.D == 3) {
+                if (t == 0 && g.halo) q[2] = hp4[((int64_t)x * g.ny + y) >> 1];
+                else q[2] = xn4[(((t == 0 ? g.T - 1 : t - 1) * (int64_t)g.nx + x) * g.ny + y) >> 1];
+            }
+            q[1] = make_float4(qy.x, qy.y, a.x, a.y);
+            (void)nxy;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if (c < g.D)
+                    eta4[c * n2 + j] = make_float4(e[c].x + ((a.x - q[c].x) - m[c].x),
+                                                   e[c].y + ((a.y - q[c].y) - m[c].y),
+                                                   e[c].z + ((a.z - q[c].z) - m[c].z),
+                                                   e[c].w + ((a.w - q[c].w) - m[c].w));
+            const float d0x = a.x - o.x, d0y = a.y - o.y, d1x = a.z - o.z, d1y = a.w - o.w;
+            v[0] += (double)d0x * d0x + (double)d0y * d0y;
+            v[1] += (double)o.x * o.x + (double)o.y * o.y;
+            v[0] += (double)d1x * d1x + (double)d1y * d1y;
+            v[1] += (double)o.z * o.z + (double)o.w * o.w;
+        }
+    } else {
     struct Px {
         float2 e[3], th[3], m[3], a, o;
     };
@@ -617,6 +658,7 @@ __global__ void __launch_bounds__(256, POST_BLOCKS_PER_SM) k_admm_post(Geom g, A
         load(h1 ? p1 : p, q1);
         use(p, q0);
         if (h1) use(p1, q1);
+    }
     }
     double tot[2];
     if (grid_reduce<2>(v, b.partials, b.tickets + 3, tot) && threadIdx.x == 0) {
