@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
 // latency-bound); without it (large images, bandwidth-bound) it runs at four
 // blocks per SM and k_tc_prep_x writes the operand
 template <bool XOP>
-__global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
+__global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -318,6 +318,67 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
             amax = fmaxf(amax, fmaxf(fabsf(a.x), fabsf(a.y)));
             rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
         };
+        if (!XOP && (g.ny & 1) == 0) {
+            // large images: pixel pairs (y, y+1) with 16-byte loads / stores;
+            // the arithmetic is theta_adj_at's (ThetaOf), per pixel
+            const int64_t n2 = g.n / 2;
+            const float4 *d4 = reinterpret_cast<const float4 *>(b.d);
+            const float4 *r4 = reinterpret_cast<const float4 *>(b.r);
+            const float4 *ws4 = reinterpret_cast<const float4 *>(A.ws);
+            float4 *ad4 = reinterpret_cast<float4 *>(b.ad);
+            for (int64_t j = i0; j < n2; j += stride) {
+                int t, x, y;
+                unflat(g, 2 * j, t, x, y);
+                const int64_t row = (int64_t)t * g.nx, pix = (int64_t)x * g.ny + y;
+                float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int sp = 0; sp < A.S; ++sp) {
+                    const float4 w = ws4[(((int64_t)sp * g.T + t) * nxy + pix) >> 1];
+                    f.x += w.x; f.y += w.y; f.z += w.z; f.w += w.w;
+                }
+                const int xm = x == 0 ? g.nx - 1 : x - 1, xp = x + 1 == g.nx ? 0 : x + 1;
+                const float4 dc = d4[j];
+                const float4 dxm = d4[((row + xm) * g.ny + y) >> 1];
+                const float4 dxp = d4[((row + xp) * g.ny + y) >> 1];
+                const float2 dym = b.d[(row + x) * g.ny + (y == 0 ? g.ny - 1 : y - 1)];
+                const float2 dyp = b.d[(row + x) * g.ny + (y + 2 == g.ny ? 0 : y + 2)];
+                float4 dtm = dc, dtp = dc;
+                if (g.D == 3) {
+                    const int tm = t == 0 ? g.T - 1 : t - 1, tq = t + 1 == g.T ? 0 : t + 1;
+                    dtm = d4[(((int64_t)tm * g.nx + x) * g.ny + y) >> 1];
+                    dtp = d4[(((int64_t)tq * g.nx + x) * g.ny + y) >> 1];
+                }
+                const float4 rr = r4[j];
+                // per pixel k of the pair: neighbours (x-1, x+1, y-1, y+1, t-1, t+1)
+                auto lap = [&](float2 dp, float2 xmv, float2 xpv, float2 ymv, float2 ypv,
+                               float2 tmv, float2 tpv) {
+                    float2 r = cadd(csub(csub(dp, xmv), csub(xpv, dp)),
+                                    csub(csub(dp, ymv), csub(ypv, dp)));
+                    if (g.D == 3) r = cadd(r, csub(csub(dp, tmv), csub(tpv, dp)));
+                    return r;
+                };
+                const float2 p0 = make_float2(dc.x, dc.y), p1 = make_float2(dc.z, dc.w);
+                const float2 l0 = lap(p0, make_float2(dxm.x, dxm.y), make_float2(dxp.x, dxp.y),
+                                      dym, p1, make_float2(dtm.x, dtm.y), make_float2(dtp.x, dtp.y));
+                const float2 l1 = lap(p1, make_float2(dxm.z, dxm.w), make_float2(dxp.z, dxp.w),
+                                      p0, dyp, make_float2(dtm.z, dtm.w), make_float2(dtp.z, dtp.w));
+                const float2 a0 = make_float2(f.x + b.hb * l0.x, f.y + b.hb * l0.y);
+                const float2 a1 = make_float2(f.z + b.hb * l1.x, f.w + b.hb * l1.y);
+                ad4[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
+                // use() without its store, pixel 0 then pixel 1
+                for (int k = 0; k < 2; ++k) {
+                    const float2 a = k ? a1 : a0, d = k ? p1 : p0;
+                    const float2 r = k ? make_float2(rr.z, rr.w) : make_float2(rr.x, rr.y);
+                    v[0] += (double)d.x * a.x + (double)d.y * a.y;
+                    v[1] += (double)d.x * a.y - (double)d.y * a.x;
+                    v[2] += (double)r.x * a.x + (double)r.y * a.y;
+                    v[3] += (double)r.x * a.y - (double)r.y * a.x;
+                    v[4] += (double)a.x * a.x + (double)a.y * a.y;
+                    v[5] += (double)r.x * r.x + (double)r.y * r.y;
+                    amax = fmaxf(amax, fmaxf(fabsf(a.x), fabsf(a.y)));
+                    rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
+                }
+            }
+        } else {
         // two grid-stride pixels per trip, all loads before the stores (more
         // bytes in flight at large n); per-thread summation order unchanged
         for (int64_t i = i0; i < g.n; i += 2 * stride) {
@@ -328,6 +389,7 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
             load(hj ? j : i, a1, d1, r1);
             use(i, a0, d0, r0);
             if (hj) use(j, a1, d1, r1);
+        }
         }
         __shared__ float shm[2][32];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -440,6 +502,27 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
             if (XOP) write_x_operand(A, t, xx, y, nxy, nd, sg);
         }
     };
+    if (!XOP && (g.ny & 1) == 0) {
+        // pixel pairs with 16-byte loads / stores (update() per pixel)
+        const int64_t n2 = g.n / 2;
+        float4 *d4 = reinterpret_cast<float4 *>(b.d);
+        float4 *x4 = reinterpret_cast<float4 *>(x);
+        float4 *r4 = reinterpret_cast<float4 *>(b.r);
+        const float4 *a4 = reinterpret_cast<const float4 *>(b.ad);
+        for (int64_t j = i0; j < n2; j += stride) {
+            const float4 dv = d4[j], xv = x4[j], rv = r4[j], av = a4[j];
+            const float2 d0 = make_float2(dv.x, dv.y), d1 = make_float2(dv.z, dv.w);
+            const float2 x0 = cadd(make_float2(xv.x, xv.y), cmul(al, d0));
+            const float2 x1 = cadd(make_float2(xv.z, xv.w), cmul(al, d1));
+            const float2 r0 = cadd(make_float2(rv.x, rv.y), cmul(nal, make_float2(av.x, av.y)));
+            const float2 r1 = cadd(make_float2(rv.z, rv.w), cmul(nal, make_float2(av.z, av.w)));
+            x4[j] = make_float4(x0.x, x0.y, x1.x, x1.y);
+            r4[j] = make_float4(r0.x, r0.y, r1.x, r1.y);
+            if (go_on)
+                d4[j] = make_float4(r0.x + be * d0.x, r0.y + be * d0.y,
+                                    r1.x + be * d1.x, r1.y + be * d1.y);
+        }
+    } else
     for (int64_t i = i0; i < g.n; i += 2 * stride) {
         const int64_t j = i + stride;
         const bool hj = j < g.n;
@@ -465,7 +548,7 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_cg_tail1(CgTailArgs A) {
 //            wise); ||r||^2 partials folded by the last block (ticket) in
 //            block order -> tau and the CG activation (fin_rhs)
 template <bool XOP>
-__global__ void __launch_bounds__(256, XOP ? 2 : 4) k_admm_head(CgTailArgs A) {
+__global__ void __launch_bounds__(256, XOP ? 2 : 3) k_admm_head(CgTailArgs A) {
     pdl_enter();
     const Geom &g = A.g;
     const AdmmBufs &b = A.b;
@@ -484,7 +567,44 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_admm_head(CgTailArgs A) {
         const float2 *rho = b.rho[cur];
         float mm = 0.f, fm = 0.f;
         // pixel-major: every component of a pixel (and its fhd bound) with
-        // all loads ahead of the stores
+        // all loads ahead of the stores; large images: pixel pairs (y, y+1)
+        // with 16-byte loads / stores (theta_at's arithmetic per pixel)
+        if (!XOP && (g.ny & 1) == 0) {
+            const int64_t n2 = g.n / 2;
+            const float4 *rho4 = reinterpret_cast<const float4 *>(rho);
+            const float4 *eta4 = reinterpret_cast<const float4 *>(b.eta);
+            const float4 *fhd4 = reinterpret_cast<const float4 *>(b.fhd);
+            float4 *mu4 = reinterpret_cast<float4 *>(b.mu);
+            for (int64_t j = i0; j < n2; j += stride) {
+                int t, x, y;
+                unflat(g, 2 * j, t, x, y);
+                const int64_t row = (int64_t)t * g.nx;
+                const float4 a = rho4[j];
+                float4 q[3], e[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (c < g.D) e[c] = eta4[c * n2 + j];
+                q[0] = rho4[((row + (x == 0 ? g.nx - 1 : x - 1)) * g.ny + y) >> 1];
+                const float2 qy = rho[(row + x) * g.ny + (y == 0 ? g.ny - 1 : y - 1)];
+                q[1] = make_float4(qy.x, qy.y, a.x, a.y);
+                if (g.D == 3)
+                    q[2] = rho4[(((t == 0 ? g.T - 1 : t - 1) * (int64_t)g.nx + x) * g.ny + y) >> 1];
+                const float4 f = fhd4[j];
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    if (c < g.D) {
+                        const float tc = c == 2 ? b.t_t : b.t_s;
+                        const float2 m0 = soft1(cadd(make_float2(a.x - q[c].x, a.y - q[c].y),
+                                                     make_float2(e[c].x, e[c].y)), tc);
+                        const float2 m1 = soft1(cadd(make_float2(a.z - q[c].z, a.w - q[c].w),
+                                                     make_float2(e[c].z, e[c].w)), tc);
+                        mu4[c * n2 + j] = make_float4(m0.x, m0.y, m1.x, m1.y);
+                        mm = fmaxf(mm, fmaxf(fabsf(m0.x - e[c].x), fabsf(m0.y - e[c].y)));
+                        mm = fmaxf(mm, fmaxf(fabsf(m1.x - e[c].z), fabsf(m1.y - e[c].w)));
+                    }
+                fm = fmaxf(fm, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
+            }
+        } else
         for (int64_t p = i0; p < g.n; p += stride) {
             int t, x, y;
             unflat(g, p, t, x, y);
@@ -557,6 +677,54 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 4) k_admm_head(CgTailArgs A) {
     {
         float2 *x = b.rho[cur ^ 1];
         MuMinusEta u{b.mu, b.eta, g, nullptr};
+        if (!XOP && (g.ny & 1) == 0) {
+            // pixel pairs: u = mu - eta at the pair and its x+1 / y+2 / t+1
+            // neighbours (theta_adj_at's arithmetic per pixel)
+            const int64_t n2 = g.n / 2;
+            const float4 *mu4 = reinterpret_cast<const float4 *>(b.mu);
+            const float4 *eta4 = reinterpret_cast<const float4 *>(b.eta);
+            const float4 *fhd4 = reinterpret_cast<const float4 *>(b.fhd);
+            float4 *x4 = reinterpret_cast<float4 *>(x);
+            float4 *r4 = reinterpret_cast<float4 *>(b.r);
+            float4 *d4 = reinterpret_cast<float4 *>(b.d);
+            auto sub4 = [](float4 m, float4 e) {
+                return make_float4(m.x - e.x, m.y - e.y, m.z - e.z, m.w - e.w);
+            };
+            for (int64_t j = i0; j < n2; j += stride) {
+                int t, xx, y;
+                unflat(g, 2 * j, t, xx, y);
+                const int64_t row = (int64_t)t * g.nx;
+                const int64_t jx = ((row + (xx + 1 == g.nx ? 0 : xx + 1)) * g.ny + y) >> 1;
+                const int64_t iy = (row + xx) * g.ny + (y + 2 == g.ny ? 0 : y + 2);
+                const float4 u0 = sub4(mu4[j], eta4[j]);
+                const float4 u0x = sub4(mu4[jx], eta4[jx]);
+                const float4 u1 = sub4(mu4[n2 + j], eta4[n2 + j]);
+                const float2 u1y = csub(b.mu[g.n + iy], b.eta[g.n + iy]);
+                float4 u2 = u0, u2t = u0;
+                if (g.D == 3) {
+                    const int64_t jt = ((((t + 1 == g.T) ? 0 : t + 1) * (int64_t)g.nx + xx) * g.ny + y) >> 1;
+                    u2 = sub4(mu4[2 * n2 + j], eta4[2 * n2 + j]);
+                    u2t = sub4(mu4[2 * n2 + jt], eta4[2 * n2 + jt]);
+                }
+                const float4 f = fhd4[j];
+                // pixel 0: y+1 neighbour is pixel 1 of the pair
+                float2 l0 = cadd(csub(make_float2(u0.x, u0.y), make_float2(u0x.x, u0x.y)),
+                                 csub(make_float2(u1.x, u1.y), make_float2(u1.z, u1.w)));
+                float2 l1 = cadd(csub(make_float2(u0.z, u0.w), make_float2(u0x.z, u0x.w)),
+                                 csub(make_float2(u1.z, u1.w), u1y));
+                if (g.D == 3) {
+                    l0 = cadd(l0, csub(make_float2(u2.x, u2.y), make_float2(u2t.x, u2t.y)));
+                    l1 = cadd(l1, csub(make_float2(u2.z, u2.w), make_float2(u2t.z, u2t.w)));
+                }
+                const float4 rhs = make_float4(f.x + b.hb * l0.x, f.y + b.hb * l0.y,
+                                               f.z + b.hb * l1.x, f.w + b.hb * l1.y);
+                x4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                r4[j] = rhs;
+                d4[j] = rhs;
+                v[0] += (double)rhs.x * rhs.x + (double)rhs.y * rhs.y;
+                v[0] += (double)rhs.z * rhs.z + (double)rhs.w * rhs.w;
+            }
+        } else
         for (int64_t i = i0; i < g.n; i += stride) {
             int t, xx, y;
             unflat(g, i, t, xx, y);
