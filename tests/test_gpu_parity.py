@@ -450,3 +450,33 @@ def test_full_size_config_operators(cuda, cfg):
     assert abs(lhs - rhs) <= 1e-6 * scale
     ga, gb = op.adjoint(y), op.adjoint(2 * y)
     assert np.array_equal(2 * ga, gb)                                          # exact scaling
+
+
+@pytest.mark.parametrize("case", ["config1", "dynamic"])
+def test_large_image_loop_kernels_at_small_size(cuda, monkeypatch, case):
+    # the large-image loop form (CG head / tail on pixel pairs without the
+    # forward operand, k_tc_prep_x before each forward) normally runs only
+    # at >= 2^22 coil-pixels (configs 3-4); CSR_XOP_SPLIT=1 forces it here so
+    # it is held to the same references as the fused form
+    monkeypatch.setenv("CSR_XOP_SPLIT", "1")
+    if case == "config1":
+        from harness.configs import make_problem
+        g = golden("admm_c1.npz")
+        prob = make_problem(1)
+        img, rep = P.admm_reconstruct(_dataset(prob.coords, prob.data), prob.sens,
+                                      P.ReconParams(**prob.params), compute_objectives=False)
+        assert rel_err(img, g["image"]) <= IMG_TOL
+        return
+    rng = np.random.default_rng(6)
+    T, nx, ny, C, m = 4, 24, 20, 3, 300
+    coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
+    sens = random_complex(rng, (C, nx, ny)) * 0.3
+    truth = random_complex(rng, (T, nx, ny))
+    op = O.Operator(coords, sens, T)
+    data = op.forward(truth)
+    kw = dict(lam=1e-3, beta=1e-2, admm_rtol=1e-150, admm_max_iters=6, cg_atol=1e-150,
+              cg_max_iters=5)
+    ref, _ = O.admm(data, coords, sens, O.Params(lam_t=5e-3, **kw), n_frames=T)
+    img, _ = P.admm_reconstruct(_dataset(coords, data, T), sens,
+                                P.ReconParams(lam_t=5e-3, **kw), compute_objectives=False)
+    assert rel_err(img, ref) <= IMG_TOL
