@@ -142,14 +142,20 @@ def pinned(arr):
 
 
 # --------------------------------------------------------------------------
+#: the CPU arm computes in the reference's precision="single" (complex64,
+#: the GPU path's arithmetic type); the f64 oracle is about 2x slower
+CPU_PRECISION = "single"
+
+
 def cpu_arm_rate(prob, n_iters):
-    """Oracle (numpy restatement of the reference, f64) ADMM it/s over
-    n_iters iterations with all host threads; returns (rate, seconds)."""
+    """Oracle (numpy/OpenBLAS restatement of the reference) ADMM it/s over
+    n_iters iterations with all host threads, in CPU_PRECISION; returns
+    (rate, seconds)."""
     from oracle import csrecon_oracle as O
     params = O.Params(**dict(prob.params, admm_max_iters=n_iters))
-    op = O.Operator(prob.coords, prob.sens, prob.n_frames, "double")
+    op = O.Operator(prob.coords, prob.sens, prob.n_frames, CPU_PRECISION)
     t0 = time.perf_counter()
-    O.admm(prob.data, prob.coords, prob.sens, params, "double", prob.n_frames, op=op)
+    O.admm(prob.data, prob.coords, prob.sens, params, CPU_PRECISION, prob.n_frames, op=op)
     dt = time.perf_counter() - t0
     return n_iters / dt, dt
 
@@ -168,11 +174,13 @@ def run_reference(args, cfg, world, rank):
     total = float(np.sum(times))
     value = args.steps / total
     sample = (f"config {cfg}: {args.steps} steps of 1 ADMM iteration (5 CG) each, "
-              f"f64 numpy/OpenBLAS oracle port of csrecon, {cores} threads")
+              f"numpy/OpenBLAS oracle port of csrecon, precision={CPU_PRECISION!r} "
+              f"(complex64), {cores} threads")
     return {"metric": METRIC, "value": value, "unit": "iter/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "c64" if CPU_PRECISION == "single" else "c128",
             "data": "synthetic (seeded BASELINE generators)",
             "config": config_dict(cfg, world),
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores,
@@ -390,7 +398,8 @@ def run_ours(args, cfg, world, rank, local):
         out["cpu_baseline"] = {"value": rate, "unit": "iter/s", "cores": cores,
                                "kind": "port",
                                "sample": f"config {cfg}, 2 ADMM iterations (5 CG each) of the "
-                                         f"f64 numpy oracle port, {dt:.1f} s"}
+                                         f"numpy oracle port, precision={CPU_PRECISION!r}, "
+                                         f"{dt:.1f} s"}
     return out if rank == 0 else None
 
 
