@@ -43,7 +43,10 @@ constexpr int TC_B_TILE = TC_BN * 128;   // 32 KiB
 constexpr int TC_STAGES = 2;
 constexpr int TC_FWD_OPS = 2 * TC_A_TILE + 2 * TC_B_TILE;  // 96 KiB / stage
 constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
-constexpr int TC_MAX_CHAIN = 24;      // max k blocks (32 samples) per accumulation chain
+#ifndef TC_CHAIN
+#define TC_CHAIN 24
+#endif
+constexpr int TC_MAX_CHAIN = TC_CHAIN;  // max k blocks (32 samples) per accumulation chain
 
 struct TcPlan {
     bool enabled = false;
