@@ -452,7 +452,7 @@ def test_full_size_config_operators(cuda, cfg):
     assert np.array_equal(2 * ga, gb)                                          # exact scaling
 
 
-@pytest.mark.parametrize("case", ["config1", "dynamic"])
+@pytest.mark.parametrize("case", ["config1", "dynamic", "dynamic_odd"])
 def test_large_image_loop_kernels_at_small_size(cuda, monkeypatch, case):
     # the large-image loop form (CG head / tail on pixel pairs without the
     # forward operand, k_tc_prep_x before each forward) normally runs only
@@ -468,7 +468,8 @@ def test_large_image_loop_kernels_at_small_size(cuda, monkeypatch, case):
         assert rel_err(img, g["image"]) <= IMG_TOL
         return
     rng = np.random.default_rng(6)
-    T, nx, ny, C, m = 4, 24, 20, 3, 300
+    # even ny: the pixel-pair kernels; odd ny: their scalar fallbacks
+    T, nx, ny, C, m = (4, 24, 20, 3, 300) if case == "dynamic" else (3, 18, 21, 5, 280)
     coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
     sens = random_complex(rng, (C, nx, ny)) * 0.3
     truth = random_complex(rng, (T, nx, ny))
