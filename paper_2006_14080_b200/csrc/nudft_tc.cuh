@@ -164,10 +164,18 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // Its split of a sample tile into pieces depends on the grid, so the
     // order-stable mode keeps the tile-group form.
     tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS") && chunk == 0;
+    // PS form of the persistent forward (A staged from shared memory next
+    // to B, two accumulators so the drain overlaps the next unit's MMAs):
+    // measured faster than A in tensor memory (config 1 39.4 vs 41.8 us,
+    // config 0 9.9 vs 11.4 us); CSR_FWD_PS=0 selects the TMEM-A form
+    {
+        const char *e = getenv("CSR_FWD_PS");
+        tc.fwd_ps = tc.fwd_ts && !(e && e[0] == '0');
+    }
     if (tc.fwd_ts) {
         const int NTt = tc.Nf / 256;
         const int64_t units = mtiles * NTt;
-        tc.fts_smem = FTS_STAGES * 2 * FTS_B_TILE + 1024 + 256;
+        tc.fts_smem = (tc.fwd_ps ? FPS_STAGES * FPS_STAGE : FTS_STAGES * 2 * FTS_B_TILE) + 1024 + 256;
         // CTAs = SMs (persistent); pieces of a sample tile split across CTAs
         // are limited to the 4 flag slots per tile
         auto max_pieces = [&](int64_t Gc) {
@@ -248,7 +256,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     cudaMemsetAsync(tc.tick, 0, 64, st);
     const int blocks = 148 * 8;
     launch(k_tc_build_fa, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.Kf, tc.fa_hi, tc.fa_lo,
-           tc.fwd_ts ? 1 : 0);
+           (tc.fwd_ts && !tc.fwd_ps) ? 1 : 0);
     launch(k_tc_build_ga, blocks, 256, 0, st, P1, T, M, tc.Mk, ny, tc.nyA, tc.ga_hi, tc.ga_lo);
     launch(k_tc_build_p0, blocks, 256, 0, st, P0, T, M, tc.Mk, nx, tc.nxp, tc.p0p);
     // max|s| (component-wise) for the image-operand scale bound
@@ -285,9 +293,12 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         tc.trace = (unsigned long long *)p;
         cudaMemsetAsync(tc.trace, 0, 4096 * 32 * 8, st);
     }
-    set_smem(k_tc_forward_ts<4>, tc.fts_smem);
-    set_smem(k_tc_forward_ts<8>, tc.fts_smem);
-    set_smem(k_tc_forward_ts<16>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<4, false>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<8, false>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<16, false>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<4, true>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<8, true>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<16, true>, tc.fts_smem);
     tc.enabled = true;
     return 0;
 }
@@ -332,9 +343,15 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.probe = tc.probe;
         dim3 grid((unsigned)tc.fts_ctas);
         switch (tc.Cp) {
-            case 4: launch(k_tc_forward_ts<4>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
-            case 8: launch(k_tc_forward_ts<8>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
-            default: launch(k_tc_forward_ts<16>, grid, FTS_THREADS, tc.fts_smem, st, tc.tm_xb256_hi, tc.tm_xb256_lo, P); break;
+#define FTS_LAUNCH(CPV)                                                                        \
+    (tc.fwd_ps ? launch(k_tc_forward_ts<CPV, true>, grid, FTS_THREADS, tc.fts_smem, st,          \
+                        tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P)             \
+               : launch(k_tc_forward_ts<CPV, false>, grid, FTS_THREADS, tc.fts_smem, st,         \
+                        tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P))
+            case 4: FTS_LAUNCH(4); break;
+            case 8: FTS_LAUNCH(8); break;
+            default: FTS_LAUNCH(16); break;
+#undef FTS_LAUNCH
         }
         if (user) {  // (T*M, C) copy for the caller
             int64_t total = (int64_t)tc.T * tc.Mk * tc.Cp;

@@ -59,6 +59,7 @@ struct TcPlan {
     int Cp = 4, xs = 32, nxp = 0, nyp = 0, nyA = 0, Kf = 0, Nf = 0;
     int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
     bool fwd_ts = false;  // A-stationary forward (2*nyp <= 256)
+    bool fwd_ps = false;  // its PS form (A from shared memory, two accumulators)
     unsigned long long *trace = nullptr;  // CSR_TRACE: per-CTA timestamps
     unsigned long long *probe = nullptr;   // [PROBE_SLOTS][4] live timing slots
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags

@@ -221,6 +221,9 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
 //   TMEM: [0,128) A_hi, [128,256) A_lo, [256,512) accumulator.
 constexpr int FTS_STAGES = 3;
 constexpr int FTS_B_TILE = 256 * 128;  // 32 KiB per hi / lo per K block (256 rows)
+// PS form: A (128 rows hi / lo) and B in every stage, two stages of 96 KiB
+constexpr int FPS_STAGES = 2;
+constexpr int FPS_STAGE = 2 * TC_A_TILE + 2 * FTS_B_TILE;
 constexpr int FTS_THREADS = 576;       // TMA, MMA, 16 epilogue (+A loader) warps
 
 struct FwdTsParams {
@@ -250,10 +253,16 @@ __device__ __forceinline__ int fts_owner(int64_t U, int G, int64_t u) {
     return b;
 }
 
-template <int CP>
+// PS = true: the same persistent unit walk with A (P1 rows) staged from
+// shared memory next to B in every K block (TMA, SW128) instead of held in
+// tensor memory, which frees TMEM for two 256-column accumulators: the
+// epilogue drains unit u while the MMAs of unit u+1 run.
+template <int CP, bool PS>
 __global__ void __launch_bounds__(FTS_THREADS, 1)
     k_tc_forward_ts(const __grid_constant__ CUtensorMap tmB_hi,
-                    const __grid_constant__ CUtensorMap tmB_lo, FwdTsParams P) {
+                    const __grid_constant__ CUtensorMap tmB_lo,
+                    const __grid_constant__ CUtensorMap tmA_hi,
+                    const __grid_constant__ CUtensorMap tmA_lo, FwdTsParams P) {
     using namespace sm100;
     // Prologue overlapped with the previous kernel (programmatic launch):
     // barrier init, TMEM allocation and the first segment's A rows read only
@@ -262,12 +271,15 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     constexpr int XQ = 32 / CP;  // x values per 64-column accumulator quarter
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    constexpr int STAGE = 2 * FTS_B_TILE;  // one K block: [hi | lo] x 256 rows
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + FTS_STAGES * STAGE);
-    uint64_t *empty = full + FTS_STAGES;
-    uint64_t *tfull = empty + FTS_STAGES;
-    uint64_t *tempty = tfull + 1;
-    uint64_t *a_ready = tempty + 1;
+    // TS: one K block = [B_hi | B_lo] x 256 rows; PS: [A_hi | A_lo | B_hi | B_lo]
+    constexpr int STAGE = PS ? FPS_STAGE : 2 * FTS_B_TILE;
+    constexpr int NSTG = PS ? FPS_STAGES : FTS_STAGES;
+    constexpr int BOFF = PS ? 2 * TC_A_TILE : 0;  // B offset in a stage
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTG * STAGE);
+    uint64_t *empty = full + NSTG;
+    uint64_t *tfull = empty + NSTG;     // [2] (PS: one per accumulator)
+    uint64_t *tempty = tfull + 2;       // [2]
+    uint64_t *a_ready = tempty + 2;
     uint64_t *a_free = a_ready + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_free + 1);
     __shared__ float2 part_acc[128][CP + 1];  // row sums folded across the quarters
@@ -284,12 +296,18 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmB_hi);
         tma_prefetch(&tmB_lo);
-        for (int s = 0; s < FTS_STAGES; ++s) {
+        if (PS) {
+            tma_prefetch(&tmA_hi);
+            tma_prefetch(&tmA_lo);
+        }
+        for (int s = 0; s < NSTG; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 16);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 16);
+        }
         mbar_init(a_ready, 16);
         mbar_init(a_free, 1);
         fence_barrier_init();
@@ -325,7 +343,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(a_ready);
     };
-    if (warp >= 2 && u0 < u1) {
+    if (!PS && warp >= 2 && u0 < u1) {
         const int q = warp & 3;
         load_a(u0 / NT, tmem + ((uint32_t)(q * 32) << 16), q * 32 + lane, (warp - 2) >> 2);
         if (tr && threadIdx.x == 64) tr[5] = gtimer();
@@ -345,15 +363,20 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                 const int nt = (int)(u - m * NT);
                 const int t = (int)(m / P.mt_per_frame);
                 const int brow = t * P.a.Nf + nt * 256;
+                const int arow = (int)m * 128;  // (T * Mk) rows of A, Mk per frame
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % FTS_STAGES;
-                    const uint32_t ph = (it / FTS_STAGES) & 1;
+                    const int s = it % NSTG;
+                    const uint32_t ph = (it / NSTG) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t *st = smem + s * STAGE;
                     mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : STAGE);
                     if (!(P.exp_flags & 2)) {
-                        tma_load_2d(st, &tmB_hi, &full[s], kb * 64, brow);
-                        tma_load_2d(st + FTS_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                        if (PS) {
+                            tma_load_2d(st, &tmA_hi, &full[s], kb * 64, arow);
+                            tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, arow);
+                        }
+                        tma_load_2d(st + BOFF, &tmB_hi, &full[s], kb * 64, brow);
+                        tma_load_2d(st + BOFF + FTS_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
                     }
                 }
             }
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             int64_t m_prev = -1;
             for (int64_t u = u0; u < u1; ++u, ++tc) {
                 const int64_t m = u / NT;
-                if (m != m_prev) {  // new segment: wait for its A
+                if (!PS && m != m_prev) {  // new segment: wait for its A
                     if (m_prev >= 0 && fwd_one()) mma_commit(a_free);  // old A is free after these MMAs
                     if (FWD_ELECT) __syncwarp();
                     mbar_wait(a_ready, seg & 1);
@@ -377,11 +400,16 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     ++seg;
                     m_prev = m;
                 }
-                mbar_wait(tempty, (tc & 1) ^ 1);  // the epilogue has read the last unit
+                // PS: accumulator ab = tc & 1 (its drain two units ago); TS:
+                // the single accumulator (the epilogue has read the last unit)
+                const int ab = PS ? (tc & 1) : 0;
+                const uint32_t tph = PS ? (((tc >> 1) & 1) ^ 1) : ((tc & 1) ^ 1);
+                mbar_wait(&tempty[ab], tph);
                 tc_fence_after();
+                const uint32_t dacc = PS ? tmem + ab * 256 : dcol;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % FTS_STAGES;
-                    const uint32_t ph = (it / FTS_STAGES) & 1;
+                    const int s = it % NSTG;
+                    const uint32_t ph = (it / NSTG) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * STAGE);
@@ -389,18 +417,26 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint32_t ac = kb * 32 + kk * 8;
-                            const uint64_t dbh = desc_sw128(st + kk * 32);
-                            const uint64_t dbl = desc_sw128(st + FTS_B_TILE + kk * 32);
+                            const uint64_t dbh = desc_sw128(st + BOFF + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + BOFF + FTS_B_TILE + kk * 32);
                             if (P.exp_flags & 1) continue;
-                            mma_f16_ts(dcol, a_hi + ac, dbh, idesc, (kb | kk) != 0);
-                            mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
-                            mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
+                            if (PS) {
+                                const uint64_t dah = desc_sw128(st + kk * 32);
+                                const uint64_t dal = desc_sw128(st + TC_A_TILE + kk * 32);
+                                mma_f16_fill(dacc, dah, dbh, idesc, (kb | kk) != 0);
+                                mma_f16_lastuse(dacc, dah, dbl, idesc, 1);
+                                mma_f16(dacc, dal, dbh, idesc, 1);
+                            } else {
+                                mma_f16_ts(dcol, a_hi + ac, dbh, idesc, (kb | kk) != 0);
+                                mma_f16_ts(dcol, a_hi + ac, dbl, idesc, 1);
+                                mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
+                            }
                         }
                         mma_commit(&empty[s]);
                     }
                     if (FWD_ELECT) __syncwarp();
                 }
-                if (fwd_one()) mma_commit(tfull);
+                if (fwd_one()) mma_commit(&tfull[ab]);
                 if (FWD_ELECT) __syncwarp();
                 if (tr && tc < 8 && lane == 0) tr[16 + tc] = gtimer();
             }
@@ -439,7 +475,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < XQ; ++i)
                     p0v[i] = valid ? p0row[xbase + i] : make_float2(0.f, 0.f);
-                if (u + 1 == ue && !last_seg) {
+                if (!PS && u + 1 == ue && !last_seg) {
                     // the segment's last unit: load the next segment's A as
                     // soon as the MMAs release the old one (the accumulator
                     // stays put meanwhile)
@@ -457,19 +493,21 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                         } while (f == 0u);
                     }
                 }
-                mbar_wait(tfull, tc & 1);
+                const int ab = PS ? (tc & 1) : 0;
+                mbar_wait(&tfull[ab], PS ? ((tc >> 1) & 1) : (tc & 1));
                 tc_fence_after();
+                const uint32_t dbase = lane_base + (PS ? ab * 256 : 256);
                 // this quarter (64 columns) in two 32-column reads; the
                 // accumulator is released right after the second read
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     uint32_t r[32];
-                    tmem_ld32(lane_base + 256 + qt * 64 + hh * 32, r);
+                    tmem_ld32(dbase + qt * 64 + hh * 32, r);
                     tmem_ld_wait();
                     if (hh == 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(tempty);
+                        if (lane == 0) mbar_arrive(&tempty[ab]);
                     }
                     if (!(P.exp_flags & 4)) {
 #pragma unroll
