@@ -348,6 +348,17 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
         load_a(u0 / NT, tmem + ((uint32_t)(q * 32) << 16), q * 32 + lane, (warp - 2) >> 2);
         if (tr && threadIdx.x == 64) tr[5] = gtimer();
     }
+    // PS: the first stages' A tiles (static factors) are fetched before
+    // pdl_wait, overlapped with the previous kernel; their B tiles after it
+    const int npre = (PS && u0 < u1 && !(P.exp_flags & 2)) ? min(NSTG, nkb) : 0;
+    if (PS && warp == 0 && lane == 0) {
+        for (int i = 0; i < npre; ++i) {
+            uint8_t *st = smem + i * STAGE;
+            mbar_arrive_expect_tx(&full[i], STAGE);
+            tma_load_2d(st, &tmA_hi, &full[i], i * 64, (int)(u0 / NT) * 128);
+            tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[i], i * 64, (int)(u0 / NT) * 128);
+        }
+    }
 
     pdl_wait();
     const bool run = !P.gate || *P.gate;
@@ -367,8 +378,13 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % NSTG;
                     const uint32_t ph = (it / NSTG) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
                     uint8_t *st = smem + s * STAGE;
+                    if (it < npre) {  // A already in flight (prologue)
+                        tma_load_2d(st + BOFF, &tmB_hi, &full[s], kb * 64, brow);
+                        tma_load_2d(st + BOFF + FTS_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                        continue;
+                    }
+                    mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], (P.exp_flags & 2) ? 0 : STAGE);
                     if (!(P.exp_flags & 2)) {
                         if (PS) {
