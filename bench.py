@@ -38,7 +38,7 @@ METRIC = "ADMM iters/s"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
 # kernel (config 1: the forward GEMM), from one `ncu --set full` capture
 # (profiles/r01_ncu_full.txt; cold cache: the factors come from HBM)
-TRAFFIC = {1: 35704576 + 256}
+TRAFFIC = {1: {"forward": 35694336 + 256, "adjoint": 35693824}}  # profiles/r01d_ncu_gemm.txt
 
 
 def peaks():
@@ -317,7 +317,7 @@ def run_ours(args, cfg, world, rank, local):
     step_ms = 1e3 * t_solve / args.steps
     roofline = {"bound": "tensor", "kernel": f"nudft_{dom}",
                 "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": TRAFFIC.get(cfg),
+                "frac": achieved / pk["bf16_tflops"], "traffic": TRAFFIC.get(cfg, {}).get(dom),
                 "peak_source": f"{src} dense bf16",
                 "flops_per_launch": flops_launch,
                 "tensor_flops_per_launch": 3 * flops_launch,
