@@ -35,10 +35,10 @@ from harness.configs import CONFIGS, make_problem, nudft_flops_per_cg  # noqa: E
 PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 METRIC = "ADMM iters/s"
-# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-# kernel (config 1: the forward GEMM), from one `ncu --set full` capture
-# (profiles/r01_ncu_full.txt; cold cache: the factors come from HBM)
-TRAFFIC = {1: {"forward": 35694336 + 256, "adjoint": 35693824}}  # profiles/r01d_ncu_gemm.txt
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of each NUDFT GEMM
+# (the roofline reports the dominant one), from one `ncu --set full`
+# capture (profiles/r01d_ncu_gemm.txt; cold cache: the factors come from HBM)
+TRAFFIC = {1: {"forward": 35694336 + 256, "adjoint": 35693824}}
 
 
 def peaks():
