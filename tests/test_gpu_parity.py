@@ -481,3 +481,45 @@ def test_large_image_loop_kernels_at_small_size(cuda, monkeypatch, case):
     img, _ = P.admm_reconstruct(_dataset(coords, data, T), sens,
                                 P.ReconParams(lam_t=5e-3, **kw), compute_objectives=False)
     assert rel_err(img, ref) <= IMG_TOL
+
+
+def test_normal_operator_hermitian_psd_and_cg_dense_oracle(cuda):
+    # test_operators.py:151-158: F^H F is Hermitian PSD; test_solver.py:62-76:
+    # CG on the normal equations against a dense solve
+    rng = np.random.default_rng(12)
+    nx, ny, nc, m = 10, 8, 3, 200
+    coords = rng.uniform(-0.5, 0.4999, size=(m, 2))
+    sens = random_complex(rng, (nc, nx, ny), np.complex64)
+    op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens)
+    x = random_complex(rng, (nx, ny), np.complex64)
+    y = random_complex(rng, (nx, ny), np.complex64)
+    ax, ay = op.normal(x, 0.02), op.normal(y, 0.02)
+    lhs = np.vdot(x.astype(complex), ay.astype(complex))
+    rhs = np.conj(np.vdot(y.astype(complex), ax.astype(complex)))
+    assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+    q = np.vdot(x.astype(complex), ax.astype(complex))
+    assert q.real > 0 and abs(q.imag) <= 1e-5 * q.real
+    # dense matrix of A = F^H F + (beta/2) Theta^H Theta, column by column
+    n = nx * ny
+    A = np.empty((n, n), complex)
+    for j in range(n):
+        e = np.zeros(n, np.complex64)
+        e[j] = 1
+        A[:, j] = op.normal(e.reshape(nx, ny), 0.02).ravel()
+    b = random_complex(rng, (nx, ny), np.complex64)
+    exact = np.linalg.solve(A, b.ravel().astype(complex)).reshape(nx, ny)
+    out = P.cg_solve(lambda v: op.normal(v, 0.02), b, None, atol=1e-12, max_iters=4 * n)
+    assert rel_err(out.solution, exact) <= 1e-3
+
+
+def test_soft_threshold_is_the_prox(cuda):
+    # test_transform.py:123-137: x = S(z, t) minimises 1/2 |x - z|^2 + t |x|
+    rng = np.random.default_rng(13)
+    z = random_complex(rng, (4096,), np.complex64)
+    t = 0.7
+    x = P.soft_threshold(z, t).astype(complex)
+    zc = z.astype(complex)
+    f = lambda v: 0.5 * np.abs(v - zc) ** 2 + t * np.abs(v)
+    for eps in (1e-3, -1e-3, 1e-3j, -1e-3j):
+        assert np.all(f(x) <= f(x + eps) + 1e-6)
+    assert np.all((np.abs(z) <= t) == (x == 0))
