@@ -108,6 +108,12 @@ __device__ __forceinline__ void all_totals(const double *part, double (&tot)[NV]
     for (int i = 0; i < NV; ++i) tot[i] = res[i];
 }
 
+// the small-image (XOP) tail also takes the pixel-pair paths (config 0 tail
+// 51.4 -> 45.6 us per iteration, config 1 44.7 -> 43.6; the head measured
+// neutral-to-slower that way and keeps the scalar form for XOP)
+#ifndef TAIL_PAIRS_XOP
+#define TAIL_PAIRS_XOP 1
+#endif
 // per-lane loads of the block-partial fold: grids of <= 32 * TAIL_FOLD blocks
 constexpr int TAIL_FOLD = 16;
 
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
             amax = fmaxf(amax, fmaxf(fabsf(a.x), fabsf(a.y)));
             rmax = fmaxf(rmax, fmaxf(fabsf(r.x), fabsf(r.y)));
         };
-        if (!XOP && (g.ny & 1) == 0) {
+        if ((!XOP || TAIL_PAIRS_XOP) && (g.ny & 1) == 0) {
             // large images: pixel pairs (y, y+1) with 16-byte loads / stores;
             // the arithmetic is theta_adj_at's (ThetaOf), per pixel
             const int64_t n2 = g.n / 2;
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
             if (XOP) write_x_operand(A, t, xx, y, nxy, nd, sg);
         }
     };
-    if (!XOP && (g.ny & 1) == 0) {
+    if ((!XOP || TAIL_PAIRS_XOP) && (g.ny & 1) == 0) {
         // pixel pairs with 16-byte loads / stores (update() per pixel)
         const int64_t n2 = g.n / 2;
         float4 *d4 = reinterpret_cast<float4 *>(b.d);
@@ -518,9 +524,16 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
             const float2 r1 = cadd(make_float2(rv.z, rv.w), cmul(nal, make_float2(av.z, av.w)));
             x4[j] = make_float4(x0.x, x0.y, x1.x, x1.y);
             r4[j] = make_float4(r0.x, r0.y, r1.x, r1.y);
-            if (go_on)
-                d4[j] = make_float4(r0.x + be * d0.x, r0.y + be * d0.y,
-                                    r1.x + be * d1.x, r1.y + be * d1.y);
+            if (go_on) {
+                const float2 n0 = make_float2(r0.x + be * d0.x, r0.y + be * d0.y);
+                const float2 n1 = make_float2(r1.x + be * d1.x, r1.y + be * d1.y);
+                d4[j] = make_float4(n0.x, n0.y, n1.x, n1.y);
+                if (XOP) {
+                    int t, xx, y;
+                    unflat(g, 2 * j, t, xx, y);
+                    write_xop2(A.a, A.sens, A.xb_hi, A.xb_lo, t, xx, y, nxy, n0, n1, sg);
+                }
+            }
         }
     } else
     for (int64_t i = i0; i < g.n; i += 2 * stride) {
