@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256, 2) k_cg_tail(CgTailArgs A) {
 // it differs from the directly summed ||r'||^2 of the reference only by the
 // fp32 rounding of r' (~1e-7 relative in beta).
 // XOP: this kernel also writes the next forward operand (small images,
-// latency-bound); without it (large images, bandwidth-bound) it runs at four
+// latency-bound); without it (large images, bandwidth-bound) it runs at three
 // blocks per SM and k_tc_prep_x writes the operand
 template <bool XOP>
 __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
