@@ -177,3 +177,25 @@ def test_cli_benchmark_single_worker_row(tmp_path):
     rows = out.read_text().strip().splitlines()
     assert rows[0] == "workers,best_seconds,speedup,ideal_speedup,note"
     assert rows[1].startswith("1,") and ",1.000,1.000," in rows[1]
+
+
+def test_shard_flag_is_validated():
+    assert _run_cli("reconstruct", "--data", "d", "--out", "x", "--shard",
+                    "tiles").returncode == 2
+
+
+@pytest.mark.gpu
+def test_cli_sample_shard_matches_library(tmp_path):
+    # --shard sample: the order-stable plan through the CLI == the library call
+    import paper_2006_14080_b200 as P
+    d, _ = _small_dataset(tmp_path)
+    out = tmp_path / "img_s.cplx"
+    assert cli.main(["reconstruct", "--data", str(d), "--out", str(out), "--admm-iters", "3",
+                     "--cg-iters", "5", "--shard", "sample"]) == 0
+    rep = json.loads((tmp_path / "img_s.cplx.report.json").read_text())
+    assert rep["timing"]["shard"] == "sample"
+    _, sens, ds, _ = load_dataset(d)
+    params = P.ReconParams(lam=1e-7, beta=1.0, admm_rtol=1e-4, admm_max_iters=3,
+                           cg_atol=1e-6, cg_max_iters=5)
+    ref, _ = P.admm_reconstruct(ds, sens, params, shard="sample", compute_objectives=False)
+    assert np.array_equal(read_tensor(out), np.asarray(ref))
