@@ -11,10 +11,12 @@ between iterations (256 MiB overwrite, outside the timed intervals), max
 over ranks.  ``e2e`` = the same metric through the public API
 (``admm_reconstruct`` with pinned host arrays: plan build, H2D, full
 reconstruction of the config's iteration count, D2H of the image).
-Multi-GPU (torchrun): coils are sharded across ranks, one NCCL allreduce of
-the image partial per CG iteration; total work is fixed -> strong scaling.
+Multi-GPU (torchrun): coils (>= 4 per rank) or samples are sharded across
+ranks, one NCCL allreduce of the image partial per CG iteration; 2-D+t
+configs shard frames; total work is fixed -> strong scaling.
 ``--impl reference`` times the CPU arm (the numpy restatement of the
-reference in oracle/, f64, all host threads) on the same config and metric.
+reference in oracle/, in the reference's precision="single", all host
+threads) on the same config and metric.
 """
 
 import argparse
