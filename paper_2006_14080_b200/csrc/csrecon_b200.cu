@@ -399,6 +399,13 @@ inline bool use_cg_tail(const csr_plan *p) {
     return !off && p->tc.enabled && !p->frame_mode && !coil_collective(p);
 }
 
+// ADMM post grid: one thread per pixel pair (even ny) or per element, at
+// most POST_BLOCKS_PER_SM blocks per SM (one wave of the grid-stride loop)
+inline int post_blocks(const Geom &g) {
+    const int64_t work = (g.ny % 2 == 0) ? g.n / 2 : g.n * g.D;
+    return std::min(ew_blocks(work), 148 * POST_BLOCKS_PER_SM);
+}
+
 int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
                            cudaStream_t st, int *nk, bool snap) {
     const Geom g = p->g;
@@ -419,7 +426,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
             if (!(skip & 8)) TRY(run_adjoint_partials(p, nullptr, st, nullptr));
             if (!(skip & 2)) TRY(launch_cg_tail(p, b, st));
         }
-        if (!(skip & 64)) launch(k_admm_post, std::min(ebD, 148 * POST_BLOCKS_PER_SM), TPB, 0, st, g, b);
+        if (!(skip & 64)) launch(k_admm_post, post_blocks(g), TPB, 0, st, g, b);
         if (!(skip & 128)) launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]);
         *nk = 0;
         return CSR_OK;
@@ -469,7 +476,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
         launch(k_stage_frames, ebf, TPB, 0, st, b, g, 1, p->sfirst, p->slast); LAUNCHED(); ++k;
         TRY(halo_exchange(p, p->sfirst, p->slast, st));
     }
-    launch(k_admm_post, std::min(ebD, 148 * POST_BLOCKS_PER_SM), TPB, 0, st, g, b); LAUNCHED(); ++k;
+    launch(k_admm_post, post_blocks(g), TPB, 0, st, g, b); LAUNCHED(); ++k;
     TRY(scalar_sync(p, b, FIN_POST, 4, 2, st, &k));
     if (snap) {  // per-iteration images only when the caller asked for them
         launch(k_snapshot, eb, TPB, 0, st, g.n, p->sc, p->rho[0], p->rho[1]); LAUNCHED(); ++k;
