@@ -174,6 +174,21 @@ def make_problem(cfg, seed=None, encoder=None):
     return Problem(cfg, nx, ny, T, C, coords, sens, data, truth, params)
 
 
+def data_probe(data):
+    """Size-independent fingerprint of a k-space array: v^T d for a fixed
+    seeded complex v (one value per coil).  The committed fixtures of the
+    large configs store it instead of the data (the GPU f64 encoder used at
+    test time reproduces the CPU encode to ~1e-12)."""
+    rng = np.random.default_rng(123)
+    v = rng.standard_normal(data.shape[0]) + 1j * rng.standard_normal(data.shape[0])
+    return v @ data
+
+
+def array_sha(arr):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
+
+
 def nudft_flops_per_cg(cfg):
     """Algorithmic NUDFT flops per CG iteration, 16*C*M_f*N*T."""
     c = CONFIGS[cfg]

@@ -102,7 +102,33 @@ typedef struct csr_plan_info {
 } csr_plan_info;
 
 int csr_plan_create(const csr_plan_desc *desc, csr_plan **out);
+/* Release a plan.  Waits for the plan's pending work on every stream it was
+ * used on (operator calls run on the caller's stream) before its memory is
+ * returned to the device pool. */
 int csr_plan_destroy(csr_plan *plan);
+
+/* A plan from the reference's own factor arrays instead of coordinates
+ * (one frame): DftOperator(factors, sens_maps, "separable")
+ * (operators.py:109-139) with the DftFactors of build_factors
+ * (operators.py:30-47, 72-82).  phase0 is P0 (M, nx); phase1 is P1 in one of
+ * the layouts the reference's kernel table passes around (kernels.py
+ * :257-262): the (M, ny) factor itself, the operator's phase1_t (ny, M)
+ * (operators.py:136) or its phase1_conj (M, ny) (operators.py:137).  All
+ * DEVICE complex64; copied into the plan. */
+#define CSR_P1_ROWS 0
+#define CSR_P1_T 1
+#define CSR_P1_CONJ 2
+typedef struct csr_factor_desc {
+    int32_t nx, ny;
+    int32_t n_coils;
+    int64_t n_samples;
+    const void *phase0;     /* (M, nx) */
+    const void *phase1;     /* layout given by phase1_layout */
+    int32_t phase1_layout;  /* CSR_P1_ROWS | CSR_P1_T | CSR_P1_CONJ */
+    const void *sens;       /* (C, nx, ny) */
+    int32_t device;
+} csr_factor_desc;
+int csr_plan_create_from_factors(const csr_factor_desc *desc, csr_plan **out);
 int csr_plan_get_info(const csr_plan *plan, csr_plan_info *info);
 
 /* Copy frame t's factors P0 (M, nx) and P1 (M, ny) (complex64) out —
@@ -117,6 +143,20 @@ int csr_forward(csr_plan *plan, const void *image, void *kdata, void *stream);
 /* DftOperator.adjoint (operators.py:195-203 -> kernels.nudft_adjoint_sep,
  * kernels.py:81-88): kdata (T*M, C) -> image (T, nx, ny); no 1/N. */
 int csr_adjoint(csr_plan *plan, const void *kdata, void *image, void *stream);
+
+/* The reference's kernel-table entries themselves (kernels.py:257-262,
+ * _forward_sep_np / _adjoint_sep_np kernels.py:71-88), all DEVICE complex64
+ * pointers: nudft_forward_sep(phase0 (M,nx), phase1_t (ny,M), sens (C,nx,ny),
+ * image (nx,ny)) -> out (M,C); nudft_adjoint_sep(phase0, phase1_conj (M,ny),
+ * sens, data (M,C)) -> out (nx,ny).  Each call builds a transient plan from
+ * the factors (csr_plan_create_from_factors) and releases it: an exact
+ * drop-in for one call; hot loops keep a plan. */
+int csr_nudft_forward_sep(const void *phase0, const void *phase1_t, const void *sens,
+                          const void *image, void *out, int32_t nx, int32_t ny,
+                          int32_t n_coils, int64_t n_samples, void *stream);
+int csr_nudft_adjoint_sep(const void *phase0, const void *phase1_conj, const void *sens,
+                          const void *data, void *out, int32_t nx, int32_t ny,
+                          int32_t n_coils, int64_t n_samples, void *stream);
 
 /* ChunkedDftOperator.adjoint (operators.py:254-265): the per-chunk partial
  * images (n_chunks, nx, ny), unsummed, of an order-stable plan
@@ -221,10 +261,13 @@ int csr_simulate_kspace(int32_t nx, int32_t ny, int32_t n_frames, int32_t n_coil
 int csr_adjoint_reconstruct(csr_plan *plan, const void *kdata, void *image,
                             void *stream);
 
-/* NCCL communicator for coil-sharded runs (replaces the thread-barrier
+/* NCCL communicator for sharded runs (replaces the thread-barrier
  * allreduce of sharding._Collective, sharding.py:211-250).  Rank 0 makes
  * the 128-byte unique id, the host broadcasts it (torch.distributed), every
- * rank creates its comm on its own device and attaches it to its plan. */
+ * rank creates its comm on its own device and attaches it to its plan.
+ * A plan with a communicator runs the collective code path of its shard
+ * mode for any rank count, one rank included (NCCL reduces / exchanges with
+ * itself), so every collective also runs on a single GPU. */
 int csr_comm_unique_id(void *id128);
 int csr_comm_create(const void *id128, int32_t nranks, int32_t rank,
                     int32_t device, csr_comm **out);

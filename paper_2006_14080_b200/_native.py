@@ -37,6 +37,16 @@ CSR_PLAN_FRAME_SHARD = 1
 CSR_PLAN_ORDERED_SAMPLES = 2
 
 
+class FactorDesc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("n_coils", ctypes.c_int32), ("n_samples", ctypes.c_int64),
+                ("phase0", ctypes.c_void_p), ("phase1", ctypes.c_void_p),
+                ("phase1_layout", ctypes.c_int32), ("sens", ctypes.c_void_p),
+                ("device", ctypes.c_int32)]
+
+CSR_P1_ROWS, CSR_P1_T, CSR_P1_CONJ = 0, 1, 2
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("factor_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("gemm_path", ctypes.c_int32), ("split_k", ctypes.c_int32)]
@@ -65,7 +75,10 @@ _I32, _I64, _F, _D = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_do
 
 SIGNATURES = {
     "csr_plan_create": [ctypes.POINTER(PlanDesc), ctypes.POINTER(_P)],
+    "csr_plan_create_from_factors": [ctypes.POINTER(FactorDesc), ctypes.POINTER(_P)],
     "csr_plan_destroy": [_P],
+    "csr_nudft_forward_sep": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I64, _P],
+    "csr_nudft_adjoint_sep": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _I64, _P],
     "csr_plan_get_info": [_P, ctypes.POINTER(PlanInfo)],
     "csr_plan_get_factors": [_P, _I32, _P, _P, _P],
     "csr_forward": [_P, _P, _P, _P],

@@ -66,8 +66,17 @@ __device__ __forceinline__ void probe_exit(unsigned long long *pr) {
     }
 }
 
+// Profiling / experiment knobs (environment variables) exist only in debug
+// builds (-DCSR_DEBUG=1: tools/build_variants.py variants loaded with
+// CSR_VARIANT); the product library never reads them, so a stray variable
+// cannot change a reconstruction.
+#ifndef CSR_DEBUG
+#define CSR_DEBUG 0
+#endif
+inline const char *dbg_env(const char *name) { return CSR_DEBUG ? getenv(name) : nullptr; }
+
 inline bool pdl_enabled() {
-    static const bool on = getenv("CSR_NO_PDL") == nullptr;
+    static const bool on = dbg_env("CSR_NO_PDL") == nullptr;
     return on;
 }
 

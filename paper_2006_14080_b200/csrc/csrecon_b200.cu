@@ -124,6 +124,7 @@ struct csr_plan {
     float *iter_ms = nullptr;
     std::vector<cudaEvent_t> iter_ev;
     std::vector<void *> allocs;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;  // caller streams (mark_use)
 };
 
 namespace {
@@ -151,7 +152,7 @@ int dalloc(csr_plan *p, T **ptr, size_t count, int64_t *acct) {
 
 // CSR_HOST_TIMING=1: host-side phase times of plan build / solve on stderr
 struct HostTimer {
-    bool on = getenv("CSR_HOST_TIMING") != nullptr;
+    bool on = dbg_env("CSR_HOST_TIMING") != nullptr;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     void mark(const char *what) {
         if (!on) return;
@@ -203,12 +204,16 @@ int run_forward(csr_plan *p, const float2 *x, float2 *out, cudaStream_t st,
 
 int nranks(const csr_plan *p) { return p->comm ? p->comm->nranks : 1; }
 
-// order-stable sample sharding across more than one rank
-bool ordered_multi(const csr_plan *p) { return p->ordered && nranks(p) > 1; }
+// A plan with a communicator attached runs the multi-rank code path for any
+// rank count (one rank included: NCCL then reduces / exchanges with itself),
+// so the collectives of every shard mode also run on a single GPU.
 
-// image partial sums over ranks need an allreduce (coil sharding)
+// order-stable sample sharding with a communicator (all-gather of chunks)
+bool ordered_multi(const csr_plan *p) { return p->ordered && p->comm; }
+
+// image partial sums over ranks need an allreduce (coil / plain sample split)
 bool coil_collective(const csr_plan *p) {
-    return !p->frame_mode && !p->ordered && nranks(p) > 1;
+    return !p->frame_mode && !p->ordered && p->comm;
 }
 
 // split-K adjoint partials into p->ws; kd == nullptr reads the internal
@@ -258,25 +263,24 @@ int run_adjoint(csr_plan *p, const float2 *kd, float2 *img, cudaStream_t st) {
 }
 
 int allreduce(csr_plan *p, float2 *buf, int64_t n_complex, cudaStream_t st) {
-    if (!p->comm || p->comm->nranks == 1) return CSR_OK;
+    if (!p->comm) return CSR_OK;
     NC(ncclAllReduce(buf, buf, (size_t)(2 * n_complex), ncclFloat, ncclSum,
                      p->comm->comm, st));
     return CSR_OK;
 }
 
-// frame-sharded plans finalise CG/ADMM scalars after an allreduce of the
-// per-rank sums (CSR_FORCE_MR exercises that path on one GPU)
-bool multi_rank_scalars(const csr_plan *p) {
-    return p->frame_mode && (nranks(p) > 1 || getenv("CSR_FORCE_MR"));
-}
+// frame-sharded plans with a communicator finalise CG/ADMM scalars after an
+// allreduce of the per-rank sums
+bool multi_rank_scalars(const csr_plan *p) { return p->frame_mode && p->comm; }
 
 // Ring halo exchange of one frame each way: hprev <- previous rank's `last`,
 // hnext <- next rank's `first` (ranks in frame order, circular like the
-// temporal difference).  One rank: local copies.
+// temporal difference).  No communicator: local copies; a one-rank
+// communicator sends to and receives from itself.
 int halo_exchange(csr_plan *p, const float2 *first, const float2 *last, cudaStream_t st) {
     const size_t nb = (size_t)p->nx * p->ny * sizeof(float2);
     const int P = nranks(p);
-    if (P == 1) {
+    if (!p->comm) {
         CU(cudaMemcpyAsync(p->hprev, last, nb, cudaMemcpyDeviceToDevice, st));
         CU(cudaMemcpyAsync(p->hnext, first, nb, cudaMemcpyDeviceToDevice, st));
         return CSR_OK;
@@ -296,7 +300,7 @@ int halo_exchange(csr_plan *p, const float2 *first, const float2 *last, cudaStre
 int scalar_sync(csr_plan *p, const AdmmBufs &b, int op, int off, int cnt, cudaStream_t st,
                 int *nk) {
     if (!b.mr) return CSR_OK;
-    if (nranks(p) > 1)
+    if (p->comm)
         NC(ncclAllReduce(p->loc + off, p->loc + off, (size_t)cnt, ncclDouble, ncclSum,
                          p->comm->comm, st));
     launch(k_finalize, 1, 1, 0, st, b, op);
@@ -339,26 +343,42 @@ AdmmBufs admm_bufs(csr_plan *p, const csr_admm_params *prm) {
 }
 
 // One ADMM iteration as a fixed kernel sequence (captured as a graph).
-// The fused CG tail (cg_tail.cuh) on a single rank with the tensor-core
-// operator; multi-rank and SIMT runs keep the separate kernels.
-int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = false) {
+// The fused CG head / tail (cg_tail.cuh) run with the tensor-core operator
+// unless the plan is frame-sharded (its CG scalars are allreduced between
+// the tail's phases); with coil / plain-sample sharding the tail reads the
+// allreduced adjoint image (ws = fhf, one partial) instead of the local
+// split-K partials.
+typedef void (*TailKernel)(CgTailArgs);
+
+TailKernel tail_kernel(const csr_plan *p, bool head) {
+    static const bool two_barriers = dbg_env("CSR_TAIL2") != nullptr;
+    if (head) return p->fuse_xop ? k_admm_head<true> : k_admm_head<false>;
+    if (two_barriers) return k_cg_tail;
+    return p->fuse_xop ? k_cg_tail1<true> : k_cg_tail1<false>;
+}
+
+int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = false,
+                   const float2 *ws = nullptr, int S = 0) {
     if (!p->tail_blocks) {
-        int per_sm = 0, sms = 0;
-        if (p->fuse_xop)
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail1<true>, TPB, 0));
-        else
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_tail1<false>, TPB, 0));
+        // one cooperative grid for the head and the tail: co-resident for
+        // the less occupant of the two kernels actually launched
+        int sms = 0, per_sm = 1 << 30;
+        for (TailKernel k : {tail_kernel(p, true), tail_kernel(p, false)}) {
+            int o = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, TPB, 0));
+            per_sm = std::min(per_sm, o);
+        }
         CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev));
         int64_t want = reduce_blocks(p->g.n * (p->C > 1 ? 2 : 1), TPB);
-        if (const char *e = getenv("CSR_TAIL_BLOCKS")) want = atoi(e);
+        if (const char *e = dbg_env("CSR_TAIL_BLOCKS")) want = atoi(e);
         // <= 32 * TAIL_FOLD blocks: the one-barrier tail folds TAIL_FOLD partials per lane
         p->tail_blocks = (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)per_sm * sms, (int64_t)32 * TAIL_FOLD}));
     }
     CgTailArgs A;
     A.g = p->g;
     A.b = b;
-    A.ws = p->ws;
-    A.S = p->S;
+    A.ws = ws ? ws : p->ws;
+    A.S = ws ? S : p->S;
     A.a = tc_args(p->tc);
     A.sens = p->sens;
     A.xb_hi = p->tc.xb_hi;
@@ -378,12 +398,7 @@ int launch_cg_tail(csr_plan *p, const AdmmBufs &b, cudaStream_t st, bool head = 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const bool two_barriers = getenv("CSR_TAIL2") != nullptr;
-    void (*kern)(CgTailArgs);
-    if (head) kern = p->fuse_xop ? k_admm_head<true> : k_admm_head<false>;
-    else if (two_barriers) kern = k_cg_tail;
-    else kern = p->fuse_xop ? k_cg_tail1<true> : k_cg_tail1<false>;
-    CU(cudaLaunchKernelEx(&cfg, kern, A));
+    CU(cudaLaunchKernelEx(&cfg, tail_kernel(p, head), A));
     LAUNCHED();
     return CSR_OK;
 }
@@ -395,8 +410,8 @@ int launch_admm_head(csr_plan *p, const AdmmBufs &b, cudaStream_t st) {
 }
 
 inline bool use_cg_tail(const csr_plan *p) {
-    static const bool off = getenv("CSR_NO_CG_TAIL") != nullptr;
-    return !off && p->tc.enabled && !p->frame_mode && !coil_collective(p);
+    static const bool off = dbg_env("CSR_NO_CG_TAIL") != nullptr;
+    return !off && p->tc.enabled && !p->frame_mode;
 }
 
 // ADMM post grid: one thread per pixel pair (even ny) or per element, at
@@ -415,7 +430,7 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     // profiling only (CSR_DBG_SKIP bits, results meaningless): 2 = CG tail,
     // 4 = forward, 8 = adjoint, 16 mu, 32 rhs, 64 post, 128 snapshot;
     // 256 = run prep_x before the first forward
-    static const int skip = getenv("CSR_DBG_SKIP") ? atoi(getenv("CSR_DBG_SKIP")) : 0;
+    static const int skip = dbg_env("CSR_DBG_SKIP") ? atoi(dbg_env("CSR_DBG_SKIP")) : 0;
     int k = 0;
     if (skip) {
         if (!(skip & 16)) launch(k_admm_mu, ebD, TPB, 0, st, g, b);
@@ -455,6 +470,13 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
         k += p->tc.enabled ? tc_forward_launches(p->tc, true, false, x_ready) : 1;
         TRY(run_adjoint_partials(p, nullptr, st, gate));
         k += p->tc.enabled ? p->tc.adj_launches : 1;
+        if (tail && coil_multi) {  // allreduce the adjoint image, then the fused tail
+            launch(k_cg_fhf, eb, TPB, 0, st, g, b, p->ws, combine_sens(p), p->S, combine_coils(p)); LAUNCHED(); ++k;
+            TRY(allreduce(p, p->fhf, g.n, st));
+            TRY(launch_cg_tail(p, b, st, false, p->fhf, 1));
+            ++k;
+            continue;
+        }
         if (tail) {
             TRY(launch_cg_tail(p, b, st));
             ++k;
@@ -509,13 +531,25 @@ extern "C" {
 const char *csr_last_error(void) { return g_err.c_str(); }
 int64_t csr_kernel_launches(void) { return g_launches.load(); }
 
-int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
+}  // extern "C"
+
+namespace {
+
+// Caller-provided device factors instead of coordinates (T == 1):
+// csr_plan_create_from_factors.
+struct FactorSource {
+    const float2 *p0 = nullptr, *p1 = nullptr;
+    int p1_layout = 0;
+};
+
+int plan_create(const csr_plan_desc *desc, const FactorSource &fs, csr_plan **out) {
     if (!desc || !out) return fail(CSR_ERR_ARG, "null argument");
     *out = nullptr;
     if (desc->nx < 1 || desc->ny < 1 || desc->n_frames < 1 || desc->n_coils < 1 ||
         desc->n_samples < 1)
         return fail(CSR_ERR_SHAPE, "plan dimensions must all be >= 1");
-    if (!desc->coords || !desc->sens) return fail(CSR_ERR_ARG, "coords and sens are required");
+    if ((!desc->coords && !fs.p0) || !desc->sens)
+        return fail(CSR_ERR_ARG, "coords (or factors) and sens are required");
     HostTimer ht;
     TRY(check_device(desc->device));
     CU(cudaSetDevice(desc->device));
@@ -573,17 +607,28 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     if ((rc = dalloc(p, &p->sens, (size_t)(p->C * nxy), &p->factor_bytes))) return cleanup(rc);
     for (auto &e : p->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "event create"));
-    // coords -> device, factors in f64 -> complex64
-    double *dcoords = nullptr;
-    if (pool_alloc((void **)&dcoords, rows * 2 * sizeof(double), st) != cudaSuccess)
-        return cleanup(fail(CSR_ERR_OOM, "coords alloc"));
-    p->allocs.push_back(dcoords);
-    if (cudaMemcpyAsync(dcoords, desc->coords, rows * 2 * sizeof(double),
-                        cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpyAsync(p->sens, desc->sens, p->C * nxy * sizeof(float2),
+    if (cudaMemcpyAsync(p->sens, desc->sens, p->C * nxy * sizeof(float2),
                         cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return cleanup(fail(CSR_ERR_CUDA, "plan upload failed"));
-    {
+    if (fs.p0) {
+        // the caller's factors (the reference's own arrays): P0 as is, P1
+        // from its layout
+        if (cudaMemcpyAsync(p->P0, fs.p0, rows * p->nx * sizeof(float2),
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return cleanup(fail(CSR_ERR_CUDA, "factor upload failed"));
+        const int blocks = (int)std::min<int64_t>((rows * p->ny + 255) / 256, 148 * 16);
+        launch(k_import_p1, blocks, 256, 0, st, fs.p1, fs.p1_layout, rows, p->ny, p->P1);
+        g_launches.fetch_add(1);
+        if (cudaGetLastError() != cudaSuccess) return cleanup(fail(CSR_ERR_CUDA, "k_import_p1 launch"));
+    } else {
+        // coords -> device, factors in f64 -> complex64
+        double *dcoords = nullptr;
+        if (pool_alloc((void **)&dcoords, rows * 2 * sizeof(double), st) != cudaSuccess)
+            return cleanup(fail(CSR_ERR_OOM, "coords alloc"));
+        p->allocs.push_back(dcoords);
+        if (cudaMemcpyAsync(dcoords, desc->coords, rows * 2 * sizeof(double),
+                            cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return cleanup(fail(CSR_ERR_CUDA, "plan upload failed"));
         int64_t total = rows * (p->nx + p->ny);
         int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
         launch(k_factors, blocks, 256, 0, st, dcoords, rows, p->nx, p->ny, p->P0, p->P1);
@@ -653,9 +698,59 @@ int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
     return CSR_OK;
 }
 
+// Record that work on `st` touches the plan's memory (csr_plan_destroy
+// waits for the latest such work on every stream used).
+int mark_use(csr_plan *p, cudaStream_t st) {
+    for (auto &u : p->uses)
+        if (u.first == st) {
+            CU(cudaEventRecord(u.second, st));
+            return CSR_OK;
+        }
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->uses.emplace_back(st, e);
+    CU(cudaEventRecord(e, st));
+    return CSR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csr_plan_create(const csr_plan_desc *desc, csr_plan **out) {
+    return plan_create(desc, FactorSource{}, out);
+}
+
+int csr_plan_create_from_factors(const csr_factor_desc *fd, csr_plan **out) {
+    if (!fd || !out) return fail(CSR_ERR_ARG, "null argument");
+    if (!fd->phase0 || !fd->phase1 || !fd->sens)
+        return fail(CSR_ERR_ARG, "phase0, phase1 and sens are required");
+    if (fd->phase1_layout < CSR_P1_ROWS || fd->phase1_layout > CSR_P1_CONJ)
+        return fail(CSR_ERR_ARG, "unknown phase1 layout");
+    csr_plan_desc d{};
+    d.nx = fd->nx;
+    d.ny = fd->ny;
+    d.n_frames = 1;
+    d.n_coils = fd->n_coils;
+    d.n_samples = fd->n_samples;
+    d.sens = fd->sens;
+    d.device = fd->device;
+    FactorSource fs;
+    fs.p0 = (const float2 *)fd->phase0;
+    fs.p1 = (const float2 *)fd->phase1;
+    fs.p1_layout = fd->phase1_layout;
+    return plan_create(&d, fs, out);
+}
+
 int csr_plan_destroy(csr_plan *p) {
     if (!p) return CSR_OK;
     cudaSetDevice(p->dev);
+    // operator calls run on the caller's streams: their work must be done
+    // before the plan's memory goes back to the pool
+    for (auto &u : p->uses) {
+        if (p->stream) cudaStreamWaitEvent(p->stream, u.second, 0);
+        else cudaEventSynchronize(u.second);
+    }
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->graph) cudaGraphExecDestroy(p->graph);
     for (void *a : p->allocs) cudaFreeAsync(a, p->stream);
@@ -664,6 +759,7 @@ int csr_plan_destroy(csr_plan *p) {
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : p->iter_ev) cudaEventDestroy(e);
+    for (auto &u : p->uses) cudaEventDestroy(u.second);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return CSR_OK;
@@ -687,19 +783,21 @@ int csr_plan_get_factors(const csr_plan *p, int32_t frame, void *p0, void *p1,
                        p->M * p->nx * sizeof(float2), cudaMemcpyDeviceToDevice, st));
     CU(cudaMemcpyAsync(p1, p->P1 + (int64_t)frame * p->M * p->ny,
                        p->M * p->ny * sizeof(float2), cudaMemcpyDeviceToDevice, st));
-    return CSR_OK;
+    return mark_use(const_cast<csr_plan *>(p), st);
 }
 
 int csr_forward(csr_plan *p, const void *image, void *kdata, void *stream) {
     if (!p || !image || !kdata) return fail(CSR_ERR_ARG, "null argument");
     CU(cudaSetDevice(p->dev));
-    return run_forward(p, (const float2 *)image, (float2 *)kdata, (cudaStream_t)stream, nullptr);
+    TRY(run_forward(p, (const float2 *)image, (float2 *)kdata, (cudaStream_t)stream, nullptr));
+    return mark_use(p, (cudaStream_t)stream);
 }
 
 int csr_adjoint(csr_plan *p, const void *kdata, void *image, void *stream) {
     if (!p || !image || !kdata) return fail(CSR_ERR_ARG, "null argument");
     CU(cudaSetDevice(p->dev));
-    return run_adjoint(p, (const float2 *)kdata, (float2 *)image, (cudaStream_t)stream);
+    TRY(run_adjoint(p, (const float2 *)kdata, (float2 *)image, (cudaStream_t)stream));
+    return mark_use(p, (cudaStream_t)stream);
 }
 
 int csr_normal(csr_plan *p, const void *x, void *out, double beta, void *stream) {
@@ -711,7 +809,7 @@ int csr_normal(csr_plan *p, const void *x, void *out, double beta, void *stream)
     k_normal_finish<<<ew_blocks(p->g.n), TPB, 0, st>>>(p->g, p->fhf, (const float2 *)x,
                                                        (float)(beta / 2), (float2 *)out);
     LAUNCHED();
-    return CSR_OK;
+    return mark_use(p, st);
 }
 
 int csr_theta(int32_t T, int32_t nx, int32_t ny, const void *img, void *diffs,
@@ -743,6 +841,46 @@ int csr_soft_threshold(const void *z, int64_t n, float t, void *out, void *strea
     return CSR_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Scratch of the standalone reductions (csr_hermitian_dot, csr_abs_sum):
+// block partials + a ticket the kernel re-arms itself, one buffer per
+// (device, stream) allocated on first use, so hot calls never allocate.
+struct ReduceScratch {
+    int dev;
+    cudaStream_t st;
+    double *buf;
+};
+std::mutex g_scratch_mu;
+std::vector<ReduceScratch> g_scratch;
+constexpr size_t SCRATCH_DOUBLES = 2 * 4 * 148;  // grid_reduce<2> over <= 4*148 blocks
+
+int reduce_scratch(cudaStream_t st, double **partials, unsigned **ticket) {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    for (auto &r : g_scratch)
+        if (r.dev == dev && r.st == st) {
+            *partials = r.buf;
+            *ticket = reinterpret_cast<unsigned *>(r.buf + SCRATCH_DOUBLES);
+            return CSR_OK;
+        }
+    double *buf = nullptr;
+    const size_t bytes = SCRATCH_DOUBLES * sizeof(double) + 16;
+    CU(cudaMalloc(&buf, bytes));
+    CU(cudaMemset(buf, 0, bytes));  // ticket starts at 0 (synchronous)
+    g_scratch.push_back({dev, st, buf});
+    *partials = buf;
+    *ticket = reinterpret_cast<unsigned *>(buf + SCRATCH_DOUBLES);
+    return CSR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int csr_hermitian_dot(const void *a, const void *b, int64_t n, double *out,
                       void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -750,16 +888,12 @@ int csr_hermitian_dot(const void *a, const void *b, int64_t n, double *out,
         CU(cudaMemsetAsync(out, 0, 2 * sizeof(double), st));
         return CSR_OK;
     }
-    int blocks = ew_blocks(n);
-    void *scratch = nullptr;
-    size_t bytes = (size_t)blocks * 2 * sizeof(double) + 16;
-    CU(cudaMallocAsync(&scratch, bytes, st));
-    unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * 2 * sizeof(double));
-    CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
-    launch(k_hdot, blocks, TPB, 0, st, (const float2 *)a, (const float2 *)b, n,
-                                   (double *)scratch, ticket, out);
+    double *partials;
+    unsigned *ticket;
+    TRY(reduce_scratch(st, &partials, &ticket));
+    launch(k_hdot, ew_blocks(n), TPB, 0, st, (const float2 *)a, (const float2 *)b, n,
+           partials, ticket, out);
     LAUNCHED();
-    CU(cudaFreeAsync(scratch, st));
     return CSR_OK;
 }
 
@@ -769,14 +903,11 @@ int csr_abs_sum(const void *z, int64_t n, double *out, void *stream) {
         CU(cudaMemsetAsync(out, 0, sizeof(double), st));
         return CSR_OK;
     }
-    int blocks = ew_blocks(n);
-    void *scratch = nullptr;
-    CU(cudaMallocAsync(&scratch, (size_t)blocks * sizeof(double) + 16, st));
-    unsigned *ticket = (unsigned *)((char *)scratch + (size_t)blocks * sizeof(double));
-    CU(cudaMemsetAsync(ticket, 0, sizeof(unsigned), st));
-    launch(k_abs_sum, blocks, TPB, 0, st, (const float2 *)z, n, (double *)scratch, ticket, out);
+    double *partials;
+    unsigned *ticket;
+    TRY(reduce_scratch(st, &partials, &ticket));
+    launch(k_abs_sum, ew_blocks(n), TPB, 0, st, (const float2 *)z, n, partials, ticket, out);
     LAUNCHED();
-    CU(cudaFreeAsync(scratch, st));
     return CSR_OK;
 }
 
@@ -796,7 +927,7 @@ int csr_adjoint_reconstruct(csr_plan *p, const void *kdata, void *image, void *s
     cudaStream_t st = (cudaStream_t)stream;
     TRY(run_adjoint(p, (const float2 *)kdata, (float2 *)image, st));
     if (coil_collective(p)) TRY(allreduce(p, (float2 *)image, p->g.n, st));
-    return CSR_OK;
+    return mark_use(p, st);
 }
 
 int csr_admm_run(csr_plan *p, const csr_admm_params *prm, const void *kdata,
@@ -1108,7 +1239,7 @@ int csr_plan_set_comm(csr_plan *p, csr_comm *c) {
     }
     if (p->ordered) {
         CU(cudaSetDevice(p->dev));
-        if (c && c->nranks > 1) {
+        if (c) {
             const int S_max = (p->n_chunks_total + c->nranks - 1) / c->nranks;
             if (p->S_local > S_max)
                 return fail(CSR_ERR_ARG, "this rank holds more chunks than an even split allows "
@@ -1150,12 +1281,53 @@ int csr_adjoint_chunks(csr_plan *p, const void *kdata, void *chunks, void *strea
     if (tc_adjoint(p->tc, (const float2 *)kdata, (float2 *)chunks, (cudaStream_t)stream, nullptr))
         return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
     g_launches.fetch_add(p->tc.adj_launches + 1, std::memory_order_relaxed);
-    return CSR_OK;
+    return mark_use(p, (cudaStream_t)stream);
+}
+
+// One-shot separable NUDFT with the reference's kernel signatures
+// (kernels.py:257-262): a transient plan from the caller's factors, one
+// application on the caller's stream, the plan released afterwards.
+static int sep_oneshot(bool fwd, const void *phase0, const void *phase1, const void *sens,
+                       const void *in, void *out, int32_t nx, int32_t ny, int32_t n_coils,
+                       int64_t n_samples, void *stream) {
+    if (!phase0 || !phase1 || !sens || !in || !out) return fail(CSR_ERR_ARG, "null argument");
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    CU(cudaStreamSynchronize(st));  // the plan build reads the factors on its own stream
+    csr_factor_desc fd{};
+    fd.nx = nx;
+    fd.ny = ny;
+    fd.n_coils = n_coils;
+    fd.n_samples = n_samples;
+    fd.phase0 = phase0;
+    fd.phase1 = phase1;
+    fd.phase1_layout = fwd ? CSR_P1_T : CSR_P1_CONJ;
+    fd.sens = sens;
+    fd.device = dev;
+    csr_plan *p = nullptr;
+    TRY(csr_plan_create_from_factors(&fd, &p));
+    const int rc = fwd ? csr_forward(p, in, out, stream) : csr_adjoint(p, in, out, stream);
+    csr_plan_destroy(p);
+    return rc;
+}
+
+int csr_nudft_forward_sep(const void *phase0, const void *phase1_t, const void *sens,
+                          const void *image, void *out, int32_t nx, int32_t ny,
+                          int32_t n_coils, int64_t n_samples, void *stream) {
+    return sep_oneshot(true, phase0, phase1_t, sens, image, out, nx, ny, n_coils, n_samples,
+                       stream);
+}
+
+int csr_nudft_adjoint_sep(const void *phase0, const void *phase1_conj, const void *sens,
+                          const void *data, void *out, int32_t nx, int32_t ny,
+                          int32_t n_coils, int64_t n_samples, void *stream) {
+    return sep_oneshot(false, phase0, phase1_conj, sens, data, out, nx, ny, n_coils, n_samples,
+                       stream);
 }
 
 int csr_comm_allreduce(csr_comm *c, void *buf, int64_t n_floats, void *stream) {
     if (!c) return fail(CSR_ERR_ARG, "null comm");
-    if (c->nranks == 1) return CSR_OK;
     CU(cudaSetDevice(c->device));
     NC(ncclAllReduce(buf, buf, (size_t)n_floats, ncclFloat, ncclSum, c->comm,
                      (cudaStream_t)stream));

@@ -59,6 +59,27 @@ __global__ void k_factors(const double *__restrict__ coords, int64_t rows,
     }
 }
 
+// Factors handed over by the caller (csr_plan_create_from_factors): P0 is
+// copied as is; P1 arrives in one of the reference's layouts (kernels.py
+// :257-262 pass phase1_t = P1^T for the forward and phase1_conj = conj(P1)
+// for the adjoint) and is stored as P1 (M, ny).
+// layout 0: P1 (M, ny); 1: P1^T (ny, M); 2: conj(P1) (M, ny)
+__global__ void k_import_p1(const float2 *__restrict__ src, int layout, int64_t M, int ny,
+                            float2 *__restrict__ P1) {
+    pdl_enter();
+    const int64_t total = M * ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i / ny;
+        const int y = (int)(i - k * ny);
+        float2 v;
+        if (layout == 1) v = src[(int64_t)y * M + k];
+        else v = src[i];
+        if (layout == 2) v.y = -v.y;
+        P1[i] = v;
+    }
+}
+
 // ---- circular finite differences ----------------------------------------
 // hprev (halo mode): the previous rank's last frame, used as frame -1
 __device__ __forceinline__ float2 theta_at(const float2 *__restrict__ v,

@@ -136,7 +136,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
                          std::vector<void *> &allocs, int64_t chunk = 0,
                          int64_t M_global = 0) {
     tc.enabled = false;
-    if (C > 16 || getenv("CSR_DISABLE_TC")) return 0;
+    if (C > TC_MAX_COILS || dbg_env("CSR_DISABLE_TC")) return 0;
     if (!get_encode()) return 0;
     tc.T = T; tc.nx = nx; tc.ny = ny; tc.C = C; tc.M = M;
     int Cp = 4;
@@ -163,13 +163,15 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // by waves x per-CTA time (tiles x K blocks x ~768 MMA cycles + setup).
     // Its split of a sample tile into pieces depends on the grid, so the
     // order-stable mode keeps the tile-group form.
-    tc.fwd_ts = tc.Kf <= 256 && !getenv("CSR_FWD_SS") && chunk == 0;
+    // (<= 16 coils: the persistent form's 576-thread CTA keeps CP complex
+    // accumulators per epilogue thread in registers)
+    tc.fwd_ts = tc.Kf <= 256 && Cp <= 16 && !dbg_env("CSR_FWD_SS") && chunk == 0;
     // PS form of the persistent forward (A staged from shared memory next
     // to B, two accumulators so the drain overlaps the next unit's MMAs):
     // measured faster than A in tensor memory (config 1 39.4 vs 41.8 us,
     // config 0 9.9 vs 11.4 us); CSR_FWD_PS=0 selects the TMEM-A form
     {
-        const char *e = getenv("CSR_FWD_PS");
+        const char *e = dbg_env("CSR_FWD_PS");
         tc.fwd_ps = tc.fwd_ts && !(e && e[0] == '0');
     }
     if (tc.fwd_ts) {
@@ -206,7 +208,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // (waves of 148 CTAs x per-CTA time: blocks x ~768 MMA cycles + chain
     // drains + CTA setup/fill), bounded by the partial-image memory.
     int S = tc_split_model(tiles, tc.kb_total, (int64_t)T * nx * ny * 8);
-    if (const char *e = getenv("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
+    if (const char *e = dbg_env("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
     if (chunk > 0) tc.kb_per_split = (int)(chunk / 32);
     S = (tc.kb_total + tc.kb_per_split - 1) / tc.kb_per_split;
@@ -217,7 +219,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     {
         const int fixed = ADJ_STAGES * ADJ_B_STAGE + 1024 + 512;
         tc.adj_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
-        if (const char *e = getenv("CSR_ADJ_NRAW"))
+        if (const char *e = dbg_env("CSR_ADJ_NRAW"))
             tc.adj_nraw = std::max(1, std::min(tc.adj_nraw, atoi(e)));
         tc.adj_smem = fixed + tc.adj_nraw * tc.adj_stage;
     }
@@ -281,14 +283,16 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem); break;
         case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem); break;
         case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
+        case 32: set_smem(k_tc_forward<32>, tc.fwd_smem); set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
+        case 64: set_smem(k_tc_forward<64>, tc.fwd_smem); set_smem(k_tc_adjoint<64>, tc.adj_smem); break;
         default: break;
     }
     if (tc_alloc(allocs, &p, PROBE_SLOTS * 4 * sizeof(unsigned long long), ws_bytes, st)) return 2;
     tc.probe = (unsigned long long *)p;
     cudaMemsetAsync(tc.probe, 0, PROBE_SLOTS * 4 * sizeof(unsigned long long), st);
-    tc.fexp = getenv("CSR_FEXP") ? atoi(getenv("CSR_FEXP")) : 0;
-    tc.aexp = getenv("CSR_EXP") ? atoi(getenv("CSR_EXP")) : 0;
-    if (getenv("CSR_TRACE")) {
+    tc.fexp = dbg_env("CSR_FEXP") ? atoi(dbg_env("CSR_FEXP")) : 0;
+    tc.aexp = dbg_env("CSR_EXP") ? atoi(dbg_env("CSR_EXP")) : 0;
+    if (dbg_env("CSR_TRACE")) {
         if (tc_alloc(allocs, &p, 4096 * 32 * 8, ws_bytes, st)) return 2;
         tc.trace = (unsigned long long *)p;
         cudaMemsetAsync(tc.trace, 0, 4096 * 32 * 8, st);
@@ -381,11 +385,14 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.scales = tc.scales;
         P.gate = gate;
         P.probe = tc.probe;
+        P.exp_flags = tc.fexp;
         dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
         switch (tc.Cp) {
             case 4: launch(k_tc_forward<4>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
             case 8: launch(k_tc_forward<8>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            default: launch(k_tc_forward<16>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            case 16: launch(k_tc_forward<16>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            case 32: launch(k_tc_forward<32>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            default: launch(k_tc_forward<64>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
         }
     }
     if (!direct) {
@@ -453,7 +460,9 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     switch (tc.Cp) {
         case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
         case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<8>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 16: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        case 32: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<32>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<64>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
     }
     if (e != cudaSuccess) return 3;
     {

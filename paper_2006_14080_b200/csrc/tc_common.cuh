@@ -47,6 +47,9 @@ constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
 #define TC_CHAIN 24
 #endif
 constexpr int TC_MAX_CHAIN = TC_CHAIN;  // max k blocks (32 samples) per accumulation chain
+// coils a tensor-core plan holds (padded to CP = 4, 8, ..., 64: 64 / CP x
+// values per adjoint tile row block, >= 1); more go to the SIMT kernels
+constexpr int TC_MAX_COILS = 64;
 
 struct TcPlan {
     bool enabled = false;

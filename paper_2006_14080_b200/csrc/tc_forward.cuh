@@ -28,6 +28,7 @@ struct FwdParams {
     float2 *kdp;  // [G][T][Mk][Cp]
     const float *scales;
     const int *gate;
+    int exp_flags;  // profiling (debug builds, CSR_FEXP): 1 no MMA, 2 no TMA
 };
 
 
@@ -86,6 +87,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                     const uint32_t ph = (it / TC_STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t *st = smem + s * TC_FWD_OPS;
+                    if (P.exp_flags & 2) {
+                        mbar_arrive(&full[s]);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[s], TC_FWD_OPS);
                     tma_load_2d(st, &tmA_hi, &full[s], kb * 64, mtile * TC_BM);
                     tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, mtile * TC_BM);
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                     if (fwd_ss_one()) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
+                            if (P.exp_flags & 1) break;
                             const uint32_t o = kk * 32;
                             const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
                             const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);

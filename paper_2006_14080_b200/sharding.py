@@ -216,7 +216,12 @@ class NcclComm:
 
     def __init__(self, rank, world, device, group=None):
         self.rank, self.world, self.device = rank, world, device
-        uid = ctypes.create_string_buffer(broadcast_unique_id(rank, group), 128)
+        if world == 1:  # a one-rank communicator needs no rendezvous
+            raw = ctypes.create_string_buffer(128)
+            _native.call("csr_comm_unique_id", raw)
+            uid = ctypes.create_string_buffer(bytes(raw.raw), 128)
+        else:
+            uid = ctypes.create_string_buffer(broadcast_unique_id(rank, group), 128)
         self.handle = ctypes.c_void_p()
         _native.call("csr_comm_create", uid, world, rank, device,
                      ctypes.byref(self.handle))

@@ -16,6 +16,7 @@ their own loops).
 
 import ctypes
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -331,10 +332,35 @@ def shard_inputs(coords, data, maps, n_frames, spec):
             np.asarray(maps)[c0:c1])
 
 
-class _Shard:
-    """This rank's operator, data and communicator (one GPU per rank)."""
+COLLECTIVES = ("auto", "nccl")
 
-    def __init__(self, dataset, sens, n_workers, op_mode, device, shard="auto"):
+
+def resolve_shard(shard, order_stable, n_frames, world):
+    """The reference's default ``order_stable=True`` makes the reduced image
+    bitwise independent of n_workers (solver.py:281-297).  For a static
+    problem on several ranks, shard="auto" therefore picks the order-stable
+    sample split; an explicit coil / plain-sample split is reduced by an
+    NCCL sum whose bits depend on the rank count, which is reported."""
+    if shard == "auto" and order_stable and n_frames == 1 and world > 1:
+        return "sample"
+    if order_stable and world > 1 and shard in ("coil", "split"):
+        warnings.warn(f"shard={shard!r} reduces partial images with an NCCL sum: the image "
+                      "is not bitwise independent of n_workers (order_stable=True asks for "
+                      "that; use shard='sample' or pass order_stable=False)", stacklevel=3)
+    return shard
+
+
+class _Shard:
+    """This rank's operator, data and communicator (one GPU per rank).
+
+    collective="nccl" attaches an NCCL communicator even at one rank, so the
+    shard mode's collective path (allreduce, halo exchange, scalar sums,
+    all-gather) runs on a single GPU; "auto" attaches one when world > 1."""
+
+    def __init__(self, dataset, sens, n_workers, op_mode, device, shard="auto",
+                 collective="auto"):
+        if collective not in COLLECTIVES:
+            raise ValueError(f"collective must be one of {COLLECTIVES}, got {collective!r}")
         maps = np.asarray(getattr(sens, "maps", sens))
         rank, world = dist_world()
         if n_workers != world:
@@ -353,7 +379,7 @@ class _Shard:
         self.data = _dev.torch.from_numpy(
             np.ascontiguousarray(ld.astype(np.complex64))).to(self.op.device)
         self.comm = None
-        if world > 1:
+        if world > 1 or collective == "nccl":
             self.comm = NcclComm(rank, world, self.op.device.index)
             _native.call("csr_plan_set_comm", self.op.plan, self.comm.handle)
 
@@ -376,7 +402,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                      op_mode="auto", memory_budget=DEFAULT_MEMORY_BUDGET,
                      compute_objectives=True, order_stable=True,
                      barrier_timeout=600.0, device=None, return_device=False,
-                     shard="auto"):
+                     shard="auto", collective="auto"):
     """Sharded ADMM reconstruction (solver.py:274-360). Returns (image, RunReport).
 
     n_workers must equal the torch.distributed world size (one process per
@@ -387,15 +413,22 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
     shard="sample" is the reference's order-stable sample split: every rank
     owns a run of whole global sample chunks, the chunk partials are
     all-gathered and folded in chunk order, and the image is bitwise the same
-    for every n_workers (order_stable, solver.py:281-297).  Objectives are
-    evaluated after the solve from per-iteration device snapshots and are
-    not timed.
+    for every n_workers (order_stable, solver.py:281-297); it is what
+    shard="auto" means for a static problem on several ranks while
+    order_stable=True (the reference's default).  Objectives are evaluated
+    after the solve from per-iteration device snapshots and are not timed.
+    collective="nccl" runs the shard mode's NCCL collectives even on one
+    rank (see _Shard).
+
+    precision: "single" (complex64) is the only arithmetic here; the
+    reference's default "double" raises.
     """
     params = ReconParams() if params is None else params
     validate_precision(precision)
     _check_inputs(dataset, sens)
     t0 = time.perf_counter()
-    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard)
+    shard = resolve_shard(shard, order_stable, _frames(dataset), dist_world()[1])
+    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard, collective)
     op, dev = sh.op, sh.op.device
     n_it = params.admm_max_iters
     rho = _dev.empty_c64(op.image_shape, dev)
@@ -413,7 +446,7 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
                 "cg_final_residual_sq": log[i].cg_final_residual_sq}
                for i in range(stats.n_iterations)]
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode in ("coil", "sample", "split"):
+    if sh.comm is not None and sh.spec.mode in ("coil", "sample", "split"):
         cs.record("setup", op.nx * op.ny * op.n_frames, calls=2)
         cs.record("solve", op.nx * op.ny * op.n_frames,
                   calls=stats.allreduce_calls - 2)
@@ -451,19 +484,20 @@ def admm_reconstruct(dataset, sens, params=None, n_workers=1, precision="single"
 def adjoint_reconstruct(dataset, sens, n_workers=1, precision="single",
                         op_mode="auto", memory_budget=DEFAULT_MEMORY_BUDGET,
                         order_stable=True, barrier_timeout=600.0, device=None,
-                        return_device=False, shard="auto"):
+                        return_device=False, shard="auto", collective="auto"):
     """Unregularised adjoint image F^H d (solver.py:363-406)."""
     validate_precision(precision)
     _check_inputs(dataset, sens)
     t0 = time.perf_counter()
-    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard)
+    shard = resolve_shard(shard, order_stable, _frames(dataset), dist_world()[1])
+    sh = _Shard(dataset, sens, n_workers, op_mode, device, shard, collective)
     op, dev = sh.op, sh.op.device
     img = _dev.empty_c64(op.image_shape, dev)
     _native.call("csr_adjoint_reconstruct", op.plan, sh.data.data_ptr(), img.data_ptr(),
                  _dev.stream_ptr(dev))
     _dev.torch.cuda.current_stream(dev).synchronize()
     cs = CommStats()
-    if sh.world > 1 and sh.spec.mode in ("coil", "sample", "split"):
+    if sh.comm is not None and sh.spec.mode in ("coil", "sample", "split"):
         cs.record("setup", op.nx * op.ny * op.n_frames)
     report = RunReport(
         method="adjoint", precision=precision, n_workers=n_workers, op_mode=op.mode,

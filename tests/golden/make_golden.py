@@ -8,7 +8,8 @@ box, whose tests only read the committed .npz files):
 The reference is copied to /tmp/refpkg first (it JIT-caches numba code and
 must never run in place) and imported from there.  Every
 fixture records reference outputs for seeded inputs; ``--big`` adds the
-config-1 ADMM run (~1 min on 8 cores).
+config-1 ADMM run (~1 min on 8 cores) and the truncated (3-iteration)
+config 2-4 runs (config 4: ~10 min on 8 cores).
 """
 
 import argparse
@@ -160,6 +161,59 @@ def gen_admm_config(cs, cfg):
          solve_seconds=rep.timing["solve_seconds"], workers=os.cpu_count())
 
 
+#: truncated ADMM fixtures of the large BASELINE configs:
+#: 3 ADMM iterations at CG = 5; frames stored for the 2-D+t configs
+TRUNC_ITERS = 3
+
+
+def trunc_frames(n_frames):
+    return sorted({0, n_frames // 2, n_frames - 1})
+
+
+def data_probe(data):
+    """Size-independent fingerprint of a k-space array: v^T d for a fixed
+    seeded complex v (C values).  The GPU f64 encoder reproduces the CPU one
+    to ~1e-12, so the tests compare probes instead of shipping the data."""
+    v = rc(np.random.default_rng(123), data.shape[0])
+    return v @ data
+
+
+def gen_admm_trunc(cs, cfg):
+    """Config 2: the reference's own admm_reconstruct (f64).  Configs 3-4
+    (2-D+t, no reference path): the f64 restatement in oracle/.  Inputs from
+    harness.configs.make_problem (CPU f64 encode)."""
+    import time
+    sys.path.insert(0, REPO)
+    from harness.configs import make_problem
+    prob = make_problem(cfg)
+    params = dict(prob.params, admm_max_iters=TRUNC_ITERS)
+    t0 = time.perf_counter()
+    if prob.n_frames == 1:
+        from csrecon.acquisition import KSpaceDataset, SensitivityMaps, Trajectory
+        from csrecon.solver import ReconParams, admm_reconstruct
+        traj = Trajectory(prob.coords, prob.coords.shape[0], 1)
+        img, rep = admm_reconstruct(KSpaceDataset(prob.data, traj),
+                                    SensitivityMaps(prob.sens), ReconParams(**params),
+                                    n_workers=os.cpu_count(), precision="double",
+                                    compute_objectives=False)
+        recs, source = rep.iterations, "reference csrecon.admm_reconstruct, f64"
+        frames = [0]
+        img = img[None]
+    else:
+        from oracle import csrecon_oracle as O
+        img, recs = O.admm(prob.data, prob.coords, prob.sens, O.Params(**params),
+                           "double", prob.n_frames)
+        source = "oracle/csrecon_oracle.admm (2-D+t restatement), f64"
+        frames = trunc_frames(prob.n_frames)
+        img = img[frames]
+    save(f"admm_trunc_c{cfg}.npz", image=img, frames=np.array(frames),
+         alpha=np.array([r["alpha"] for r in recs]),
+         tau=np.array([r["cg_final_residual_sq"] for r in recs]),
+         iters=TRUNC_ITERS, source=source, data_probe=data_probe(prob.data),
+         sha_sens=sha(prob.sens), sha_coords=sha(prob.coords), sha_truth=sha(prob.truth),
+         seconds=time.perf_counter() - t0, workers=os.cpu_count())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -171,6 +225,8 @@ def main():
             "c0": lambda c: gen_admm_config(c, 0)}
     if args.big:
         jobs["c1"] = lambda c: gen_admm_config(c, 1)
+        for cfg in (2, 3, 4):
+            jobs[f"t{cfg}"] = lambda c, cfg=cfg: gen_admm_trunc(c, cfg)
     for name, fn in jobs.items():
         if args.only and name not in args.only.split(","):
             continue

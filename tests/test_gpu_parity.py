@@ -76,8 +76,12 @@ def test_operator_random_shapes_vs_direct_sum(cuda):
     (40, 320, 3, 1800),    # two full tiles + a half tile, padded coils
     (32, 200, 16, 1500),   # ny % 128 = 72, 16 coils
     (96, 136, 5, 2048),    # ny % 128 = 8: a mostly empty last tile
+    (64, 64, 32, 3000),    # 32 coils: CP = 32 tensor-core tiles (2 x per adjoint row block)
+    (40, 96, 48, 2000),    # 48 coils padded to CP = 64 (one x per adjoint row block)
+    (24, 20, 66, 700),     # > 64 coils: the SIMT kernels
 ])
 def test_operator_tile_shapes_vs_oracle(cuda, nx, ny, nc, m):
+    op_path = "simt" if nc > 64 else "tcgen05"
     # ragged adjoint y tiles (128 pixel rows, zero-padded factor rows) and
     # forward K padding; both operators vs the f64 separable restatement
     # (kernels.py:71-88)
@@ -88,6 +92,7 @@ def test_operator_tile_shapes_vs_oracle(cuda, nx, ny, nc, m):
     y = random_complex(rng, (m, nc))
     p0, p1 = O.build_factors(coords, nx, ny, "double")
     op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens.astype(np.complex64))
+    assert op.info()["gemm_path"] == op_path
     ef = rel_err(op.forward(img.astype(np.complex64)), O.forward_sep(p0, p1, sens, img))
     ea = rel_err(op.adjoint(y.astype(np.complex64)), O.adjoint_sep(p0, p1, sens, y))
     assert ef <= OP_TOL, ef
@@ -271,12 +276,11 @@ def test_dynamic_matches_oracle(cuda):
     assert rel_err(gpu_op.forward(truth.astype(np.complex64)), data) <= OP_TOL
 
 
-@pytest.mark.parametrize("force_mr", [False, True])
-def test_frame_shard_path_matches_oracle(cuda, force_mr, monkeypatch):
-    # the frame-sharded loop (halo frames, scalars finalised after the
-    # allreduce) on one rank: halos come from the rank itself
-    if force_mr:
-        monkeypatch.setenv("CSR_FORCE_MR", "1")
+@pytest.mark.parametrize("collective", ["auto", "nccl"])
+def test_frame_shard_path_matches_oracle(cuda, collective):
+    # the frame-sharded loop (halo frames; with a communicator, scalars
+    # finalised after the NCCL allreduce) on one rank: halos come from the
+    # rank itself
     rng = np.random.default_rng(9)
     T, nx, ny, C, m = 3, 20, 16, 3, 250
     coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
@@ -288,7 +292,7 @@ def test_frame_shard_path_matches_oracle(cuda, force_mr, monkeypatch):
     ref, _ = O.admm(data, coords, sens, O.Params(lam_t=5e-3, **kw), n_frames=T)
     img, rep = P.admm_reconstruct(_dataset(coords, data, T), sens,
                                   P.ReconParams(lam_t=5e-3, **kw), shard="frame",
-                                  compute_objectives=False)
+                                  collective=collective, compute_objectives=False)
     assert rep.timing["shard"] == "frame"
     assert rel_err(img, ref) <= IMG_TOL
 
@@ -530,6 +534,8 @@ def test_soft_threshold_is_the_prox(cuda):
     (1, 33, 17, 16, 400),   # 16 coils (the widest operand), odd sizes
     (1, 1, 24, 3, 60),      # degenerate 1 x ny image
     (2, 12, 10, 5, 130),    # 2-D+t, two frames
+    (1, 40, 36, 32, 900),   # 32 coils (CP = 32 tensor-core path)
+    (1, 20, 18, 66, 300),   # 66 coils: the SIMT path through the native loop
 ])
 def test_admm_shapes_vs_oracle(cuda, T, nx, ny, C, m):
     # the native loop (head, forward, adjoint, tail, post) on ragged / extreme
