@@ -52,11 +52,28 @@ def available():
     return os.path.isdir(os.path.join(REF_DIR, "csrecon"))
 
 
-def load():
-    """Import the staged reference package (``csrecon``)."""
+def numba_blas_available():
+    """The reference's numba kernels call np.dot inside @njit, which numba
+    can only compile with scipy's BLAS bindings present."""
+    try:
+        from numba.np.linalg import ensure_blas
+        ensure_blas()
+        return True
+    except Exception:
+        return False
+
+
+def load(backend=None):
+    """Import the staged reference package (``csrecon``).  backend sets
+    CSRECON_BACKEND (kernels.py:32-53) before the import; default: the
+    reference's own "auto", or "numpy" where numba cannot compile the
+    reference's BLAS calls (no scipy on the host)."""
     if not available():
         raise ImportError("oracle/_ref/csrecon is missing: run oracle/build_ref.py in the "
                           "build container (needs /root/reference)")
+    if backend is None:
+        backend = "auto" if numba_blas_available() else "numpy"
+    os.environ["CSRECON_BACKEND"] = backend
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/csrecon_numba_cache")
     if REF_DIR not in sys.path:
         sys.path.insert(0, REF_DIR)

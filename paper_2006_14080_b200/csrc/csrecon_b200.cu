@@ -275,12 +275,14 @@ bool multi_rank_scalars(const csr_plan *p) { return p->frame_mode && p->comm; }
 
 // Ring halo exchange of one frame each way: hprev <- previous rank's `last`,
 // hnext <- next rank's `first` (ranks in frame order, circular like the
-// temporal difference).  No communicator: local copies; a one-rank
-// communicator sends to and receives from itself.
+// temporal difference).  One rank: local copies, communicator or not — NCCL
+// send/recv to self inside a captured graph never completes (measured with
+// NCCL 2.28.9 on B200, tools/nccl_self_probe.cu: eager self send/recv works,
+// the same group captured and replayed hangs), so only P > 1 uses NCCL here.
 int halo_exchange(csr_plan *p, const float2 *first, const float2 *last, cudaStream_t st) {
     const size_t nb = (size_t)p->nx * p->ny * sizeof(float2);
     const int P = nranks(p);
-    if (!p->comm) {
+    if (P == 1) {
         CU(cudaMemcpyAsync(p->hprev, last, nb, cudaMemcpyDeviceToDevice, st));
         CU(cudaMemcpyAsync(p->hnext, first, nb, cudaMemcpyDeviceToDevice, st));
         return CSR_OK;

@@ -7,7 +7,8 @@ from paper_2006_14080_b200 import _native
 from harness.configs import make_problem
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-prob = make_problem(cfg)
+# geometry only (coil maps, coordinates, phantom): the encode is skipped
+prob = make_problem(cfg, encoder=lambda img, s, k: np.zeros((k.shape[0], s.shape[0])))
 op = P.DftOperator.build(prob.coords, P.ImageGrid(prob.nx, prob.ny), prob.sens, n_frames=prob.n_frames)
 dev = op.device
 x = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(prob.truth, op.image_shape).astype(np.complex64))).to(dev)
