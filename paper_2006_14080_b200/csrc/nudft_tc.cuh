@@ -3,6 +3,7 @@
 #pragma once
 
 #include "tc_adjoint.cuh"
+#include "tc_adjoint_w.cuh"
 #include "tc_forward.cuh"
 
 namespace csr {
@@ -79,17 +80,18 @@ inline void set_smem(F kernel, int bytes) {
 }
 
 // Adjoint split-K cost model: waves of 148 CTAs x per-CTA time (blocks x
-// ~768 MMA cycles + chain drains + CTA setup/fill), bounded by the
+// blk_cycles of MMA + chain drains + CTA setup/fill), bounded by the
 // partial-image memory; returns the number of k ranges S.
-inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes) {
+inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes, int blk_cycles = 768,
+                          int chain = TC_MAX_CHAIN) {
     int S = 1;
     int64_t best_cost = INT64_MAX;
     for (int c = 1; c <= std::min(kb_total, 1024); ++c) {
         if (c > 1 && c * pix_bytes > ((int64_t)1 << 30)) break;
         const int64_t kbps = (kb_total + c - 1) / c;
-        const int64_t nch = (kbps + TC_MAX_CHAIN - 1) / TC_MAX_CHAIN;
+        const int64_t nch = (kbps + chain - 1) / chain;
         const int64_t waves = (tiles * c + 147) / 148;
-        const int64_t cost = waves * (kbps * 768 + nch * 700 + 4000);
+        const int64_t cost = waves * (kbps * blk_cycles + nch * 700 + 4000);
         if (cost < best_cost) {
             best_cost = cost;
             S = c;
@@ -98,14 +100,41 @@ inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes) {
     return S;
 }
 
+// Adjoint tile geometry.  ny <= 128 (or more than 16 coils): 128-row y tiles
+// of k_tc_adjoint.  Otherwise the wide kernel k_tc_adjoint_w: nyt tiles of
+// N rows (a multiple of 16, <= 256) covering ny, one generated operand per
+// K block for all N rows.
+struct AdjGeom {
+    bool wide = false;
+    int N = 128, nyt = 1, NA = 4, NB = 0, chain = TC_MAX_CHAIN, blk_cycles = 768;
+};
+inline AdjGeom tc_adj_geom(int ny, int Cp) {
+    AdjGeom g;
+    g.nyt = (ny + 127) / 128;
+    if (ny <= 128 || Cp > 16 || dbg_env("CSR_ADJ_NARROW")) return g;
+    g.wide = true;
+    g.nyt = (ny + ADJW_MAX_N - 1) / ADJW_MAX_N;
+    g.N = ((ny + g.nyt - 1) / g.nyt + 15) / 16 * 16;
+    // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128)
+    g.NA = std::min(4, (512 - g.N - (g.N - 128)) / 64);
+    // B ring: enough stages to hold the combine's sums [N][ADJ_SUM_LD] afterwards
+    const int bst = adjw_b_stage(g.N);
+    g.NB = std::max(2, (g.N * ADJ_SUM_LD * 4 + bst - 1) / bst);
+    // three N-wide MMAs per K step truncate into one fp32 accumulator:
+    // shorter chains than the two-accumulator kernel
+    g.chain = TC_ADJW_CHAIN;
+    if (const char *e = dbg_env("CSR_ADJW_CHAIN")) g.chain = std::max(1, atoi(e));
+    g.blk_cycles = 4 * 3 * (g.N / 2 + 32);
+    return g;
+}
+
 // Coil padding and adjoint tile count of a (T, nx, ny, C) plan.
 inline void tc_tiles(int T, int nx, int ny, int C, int &Cp, int64_t &tiles) {
     Cp = 4;
     while (Cp < C) Cp *= 2;
     const int xs = 128 / Cp;
     const int nxp = (nx + xs - 1) / xs * xs;
-    const int nyA = (ny + 127) / 128 * 128;
-    tiles = (int64_t)T * (nxp * Cp / 64) * (nyA / 128);
+    tiles = (int64_t)T * (nxp * Cp / 64) * tc_adj_geom(ny, Cp).nyt;
 }
 
 // Global sample-chunk grid of an order-stable sample-sharded problem
@@ -118,7 +147,8 @@ inline void tc_sample_chunking(int nx, int ny, int C, int64_t M, int64_t &chunk,
     int64_t tiles;
     tc_tiles(1, nx, ny, C, Cp, tiles);
     const int kb_total = (int)((M + 127) / 128 * 128 / 32);
-    const int S = tc_split_model(tiles, kb_total, (int64_t)nx * ny * 8);
+    const AdjGeom ag = tc_adj_geom(ny, Cp);
+    const int S = tc_split_model(tiles, kb_total, (int64_t)nx * ny * 8, ag.blk_cycles, ag.chain);
     int kbps = (kb_total + S - 1) / S;
     kbps = (kbps + 3) / 4 * 4;
     chunk = (int64_t)kbps * 32;
@@ -202,12 +232,19 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // adjoint split-K
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
-    const int64_t tiles = (int64_t)T * tc.mt_a * (tc.nyA / 128);
+    const AdjGeom ag = tc_adj_geom(ny, Cp);
+    tc.adj_w = ag.wide;
+    tc.adjw_N = ag.N;
+    tc.adjw_nyt = ag.nyt;
+    tc.adjw_NA = ag.NA;
+    tc.adjw_NB = ag.NB;
+    tc.adj_chain = ag.chain;
+    const int64_t tiles = (int64_t)T * tc.mt_a * ag.nyt;
     // split-K: each CTA takes one tile and a contiguous k range, cut into
     // accumulation chains of <= TC_MAX_CHAIN blocks.  Pick S by a cost model
     // (waves of 148 CTAs x per-CTA time: blocks x ~768 MMA cycles + chain
     // drains + CTA setup/fill), bounded by the partial-image memory.
-    int S = tc_split_model(tiles, tc.kb_total, (int64_t)T * nx * ny * 8);
+    int S = tc_split_model(tiles, tc.kb_total, (int64_t)T * nx * ny * 8, ag.blk_cycles, ag.chain);
     if (const char *e = dbg_env("CSR_TC_SPLIT")) S = std::max(1, std::min(atoi(e), tc.kb_total));
     tc.kb_per_split = (tc.kb_total + S - 1) / S;
     if (chunk > 0) tc.kb_per_split = (int)(chunk / 32);
@@ -222,6 +259,12 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         if (const char *e = dbg_env("CSR_ADJ_NRAW"))
             tc.adj_nraw = std::max(1, std::min(tc.adj_nraw, atoi(e)));
         tc.adj_smem = fixed + tc.adj_nraw * tc.adj_stage;
+    }
+    if (tc.adj_w) {
+        const int fixed = tc.adjw_NB * adjw_b_stage(tc.adjw_N) + 1024 + 512;
+        tc.adjw_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
+        tc.adjw_smem = fixed + tc.adjw_nraw * tc.adj_stage;
+        if (tc.adjw_nraw < 2) tc.adj_w = false;  // keep the narrow kernel
     }
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
@@ -276,15 +319,20 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_xb256_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 256) &&
               tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
+              (!tc.adj_w ||
+               (tmap_f16_2d(&tc.tm_gaw_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, tc.adjw_N) &&
+                tmap_f16_2d(&tc.tm_gaw_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, tc.adjw_N))) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
               tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
     if (!ok) return 0;  // descriptor encode unavailable: SIMT path
     switch (Cp) {
-        case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem); break;
-        case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem); break;
-        case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem); break;
+        case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem);
+                set_smem(k_tc_adjoint_w<4>, tc.adjw_smem); break;
+        case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem);
+                set_smem(k_tc_adjoint_w<8>, tc.adjw_smem); break;
+        case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem);
+                 set_smem(k_tc_adjoint_w<16>, tc.adjw_smem); break;
         case 32: set_smem(k_tc_forward<32>, tc.fwd_smem); set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
-        case 64: set_smem(k_tc_forward<64>, tc.fwd_smem); set_smem(k_tc_adjoint<64>, tc.adj_smem); break;
         default: break;
     }
     if (tc_alloc(allocs, &p, PROBE_SLOTS * 4 * sizeof(unsigned long long), ws_bytes, st)) return 2;
@@ -391,8 +439,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
             case 4: launch(k_tc_forward<4>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
             case 8: launch(k_tc_forward<8>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
             case 16: launch(k_tc_forward<16>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            case 32: launch(k_tc_forward<32>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            default: launch(k_tc_forward<64>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+            default: launch(k_tc_forward<32>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
         }
     }
     if (!direct) {
@@ -430,26 +477,9 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
                       const int *gate) {
     TcArgs a = tc_args(tc);
     if (user) tc_load_kd(tc, user, st);
-    AdjParams P;
-    P.a = a;
-    P.S = tc.split;
-    P.kb_per_split = tc.kb_per_split;
-    P.chain = TC_MAX_CHAIN;
-    P.exp_flags = tc.aexp;
-    P.trace = tc.trace;
-    P.probe = tc.probe ? tc.probe + 4 * PROBE_ADJ : nullptr;
-    P.kb_total = tc.kb_total;
-    P.raw_bytes = tc.raw_bytes;
-    P.n_raw = tc.adj_nraw;
-    P.sens = tc.sens;
-    P.ws = ws;
-    P.scales = tc.scales;
-    P.gate = gate;
-    dim3 grid((unsigned)tc.mt_a, (unsigned)(tc.nyA / 128), (unsigned)(tc.T * tc.split));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(ADJ_THREADS);
-    cfg.dynamicSmemBytes = tc.adj_smem;
+    cfg.blockDim = dim3(tc.adj_w ? ADJW_THREADS : ADJ_THREADS);
+    cfg.dynamicSmemBytes = tc.adj_w ? tc.adjw_smem : tc.adj_smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -457,14 +487,58 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaError_t e;
-    switch (tc.Cp) {
-        case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<8>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 16: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        case 32: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<32>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<64>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+    if (tc.adj_w) {
+        AdjWParams P;
+        P.a = a;
+        P.S = tc.split;
+        P.kb_per_split = tc.kb_per_split;
+        P.chain = tc.adj_chain;
+        P.N = tc.adjw_N;
+        P.NA = tc.adjw_NA;
+        P.NB = tc.adjw_NB;
+        P.exp_flags = tc.aexp;
+        P.probe = tc.probe ? tc.probe + 4 * PROBE_ADJ : nullptr;
+        P.kb_total = tc.kb_total;
+        P.raw_bytes = tc.raw_bytes;
+        P.n_raw = tc.adjw_nraw;
+        P.sens = tc.sens;
+        P.ws = ws;
+        P.scales = tc.scales;
+        P.gate = gate;
+        cfg.gridDim = dim3((unsigned)tc.mt_a, (unsigned)tc.adjw_nyt, (unsigned)(tc.T * tc.split));
+        switch (tc.Cp) {
+            case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<4>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
+            case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<8>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
+            default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<16>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
+        }
+    } else {
+        AdjParams P;
+        P.a = a;
+        P.S = tc.split;
+        P.kb_per_split = tc.kb_per_split;
+        P.chain = tc.adj_chain;
+        P.exp_flags = tc.aexp;
+        P.trace = tc.trace;
+        P.probe = tc.probe ? tc.probe + 4 * PROBE_ADJ : nullptr;
+        P.kb_total = tc.kb_total;
+        P.raw_bytes = tc.raw_bytes;
+        P.n_raw = tc.adj_nraw;
+        P.sens = tc.sens;
+        P.ws = ws;
+        P.scales = tc.scales;
+        P.gate = gate;
+        cfg.gridDim = dim3((unsigned)tc.mt_a, (unsigned)(tc.nyA / 128), (unsigned)(tc.T * tc.split));
+        switch (tc.Cp) {
+            case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<4>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+            case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<8>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+            case 16: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<16>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+            default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint<32>, tc.tm_ga_hi, tc.tm_ga_lo, tc.tm_p0, tc.tm_kd, P); break;
+        }
     }
-    if (e != cudaSuccess) return 3;
+    if (e != cudaSuccess) {
+        tc_last_error() = cudaGetErrorString(e);
+        return 3;
+    }
     {
         const cudaError_t le = cudaGetLastError();
         if (le != cudaSuccess) {

@@ -1,0 +1,353 @@
+// Wide-tile adjoint NUDFT on tcgen05 for images with 128 < ny (per y tile
+// up to 256 pixel rows): one CTA covers N pixel rows y (N = 144 ... 256)
+// of a 128-row (x, c, Re/Im) tile, so every generated operand value W
+// feeds 3 MMAs of width N instead of two 128-wide tiles each regenerating
+// it, and all MMAs run at N > 128 (the N = 128 correction MMA of
+// k_tc_adjoint runs at ~70 % of the per-column rate of an N = 256 one).
+//
+//   per 16-deep K step:  D += A_hi B_hi ;  D += A_hi B_lo ;  D += A_lo B_hi
+//
+// with A = the generated W' (hi / lo, from TMEM, as k_tc_adjoint) and
+// B = conj(P1)^T (hi / lo N-row tiles, TMA).  The three products share ONE
+// accumulator D (N columns), as the forward's SS form does, which leaves
+// TMEM room for the A stages and a running-sum region:
+//   TMEM: [0, N) D | [N, N + 64 NA) A stages (hi 32 | lo 32) | [.., + N-128) S
+// Chains of P.chain K blocks (shorter than k_tc_adjoint's: three MMAs per
+// K step now truncate into the same fp32 accumulator) are drained by the
+// four epilogue warps: columns [0, 128) into fp32 register sums, columns
+// [128, N) into the TMEM sum region S (tcgen05.ld D, ld S, add, st S).
+// The end of the k range goes through shared memory (over the idle B ring)
+// into the coil combine, as k_tc_adjoint.
+//
+// Roles (12 warps): 0 lane 0 B-ring TMA, lane 1 input-ring TMA; 1 MMA
+// issuer (elected lane); 2-3 input prep (d'); 4-7 generators (one per TMEM
+// lane quarter, 32 samples each); 8-11 epilogue.
+#pragma once
+
+#include "tc_adjoint.cuh"
+
+namespace csr {
+
+constexpr int ADJW_MAX_N = 256;
+constexpr int ADJW_THREADS = 12 * 32;
+
+struct AdjWParams {
+    unsigned long long *probe;
+    TcArgs a;
+    int S, kb_per_split, kb_total, raw_bytes, n_raw, chain;
+    int N;        // pixel rows per CTA (multiple of 16, 128 < N <= 256)
+    int NA;       // A stages in TMEM
+    int NB;       // B ring stages in shared memory
+    int exp_flags;
+    const float2 *sens;
+    float2 *ws;
+    const float *scales;
+    const int *gate;
+};
+
+// shared memory: B ring NB x (hi N x 128 B | lo N x 128 B), input ring,
+// barriers; the coil-combine sums [N][ADJ_SUM_LD] floats reuse the B ring
+__host__ __device__ constexpr int adjw_b_stage(int N) { return 2 * N * 128; }
+
+template <int CP>
+__global__ void __launch_bounds__(ADJW_THREADS, 1)
+    k_tc_adjoint_w(const __grid_constant__ CUtensorMap tmB_hi,
+                   const __grid_constant__ CUtensorMap tmB_lo,
+                   const __grid_constant__ CUtensorMap tmP0,
+                   const __grid_constant__ CUtensorMap tmKd, AdjWParams P) {
+    using namespace sm100;
+    pdl_trigger();
+    constexpr int XS = 64 / CP;
+    constexpr int IN_STAGE = adj_in_stage_bytes(CP);
+    constexpr int OFF_D = 32 * XS * 8, OFF_DP = OFF_D + 32 * CP * 8;
+    constexpr int GW = 4, SPW = 32;  // generator warps, samples per warp and K block
+    const int N = P.N, NA = P.NA, NB = P.NB;
+    const int BST = adjw_b_stage(N);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *in_base = smem + NB * BST;
+    float *sum_s = reinterpret_cast<float *>(smem);  // after the main loop
+    uint64_t *bfull = reinterpret_cast<uint64_t *>(in_base + P.n_raw * IN_STAGE);
+    uint64_t *bempty = bfull + 4;
+    uint64_t *gen = bempty + 4;        // [NA] A stage written
+    uint64_t *aempty = gen + 4;        // [NA] A stage consumed
+    uint64_t *rfull = aempty + 4;
+    uint64_t *dfull = rfull + ADJ_MAX_RAW;
+    uint64_t *rempty = dfull + ADJ_MAX_RAW;
+    uint64_t *acc_full = rempty + ADJ_MAX_RAW;
+    uint64_t *acc_empty = acc_full + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = blockIdx.x, nt = blockIdx.y;
+    const int t = blockIdx.z % P.a.T, s_id = blockIdx.z / P.a.T;
+    const int kb0 = s_id * P.kb_per_split;
+    const int kb1 = min(P.kb_total, kb0 + P.kb_per_split);
+    const int nkb = kb1 - kb0;
+    const int chain = P.chain;
+    const int nchain = (nkb + chain - 1) / chain;
+    const int NR = P.n_raw;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmB_hi);
+        tma_prefetch(&tmB_lo);
+        tma_prefetch(&tmP0);
+        tma_prefetch(&tmKd);
+        for (int s = 0; s < NB; ++s) {
+            mbar_init(&bfull[s], 1);
+            mbar_init(&bempty[s], 1);
+        }
+        for (int s = 0; s < NA; ++s) {
+            mbar_init(&gen[s], GW);
+            mbar_init(&aempty[s], 1);
+        }
+        for (int r = 0; r < NR; ++r) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&dfull[r], 2);
+            mbar_init(&rempty[r], GW);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 4);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t a_col0 = (uint32_t)N;                 // A stages
+    const uint32_t s_col0 = (uint32_t)(N + 64 * NA);     // running sums of cols >= 128
+    // the first B stages (static factor) before the programmatic wait
+    const int pre = min(nkb, NB);
+    const int brow = t * P.a.nyA + nt * N;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < pre; ++i) {
+            uint8_t *st = smem + i * BST;
+            mbar_arrive_expect_tx(&bfull[i], BST);
+            tma_load_2d(st, &tmB_hi, &bfull[i], (kb0 + i) * 64, brow);
+            tma_load_2d(st + N * 128, &tmB_lo, &bfull[i], (kb0 + i) * 64, brow);
+        }
+    }
+    pdl_wait();
+    const bool run = !P.gate || *P.gate;
+    if (run) probe_enter(P.probe);
+
+    if (!run) {
+        if (warp == 0 && lane == 0)
+            for (int i = 0; i < pre; ++i) mbar_wait(&bfull[i], 0);
+    } else if (warp == 0) {
+        if (lane == 0) {
+            for (int i = pre; i < nkb; ++i) {
+                const int kb = kb0 + i;
+                const int s = i % NB;
+                wait_slow(&bempty[s], ((i / NB) & 1) ^ 1);
+                uint8_t *st = smem + s * BST;
+                mbar_arrive_expect_tx(&bfull[s], BST);
+                tma_load_2d(st, &tmB_hi, &bfull[s], kb * 64, brow);
+                tma_load_2d(st + N * 128, &tmB_lo, &bfull[s], kb * 64, brow);
+            }
+        } else if (lane == 1) {
+            const uint32_t tx = P.raw_bytes;
+            for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
+                const int kb = kb0 + i;
+                wait_slow(&rempty[r], rph ^ 1);
+                uint8_t *in = in_base + r * IN_STAGE;
+                mbar_arrive_expect_tx(&rfull[r], tx);
+                tma_load_3d(in, &tmP0, &rfull[r], mt * XS, kb * 32, t);
+                tma_load_3d(in + OFF_D, &tmKd, &rfull[r], 0, kb * 32, t);
+                if (++r == NR) {
+                    r = 0;
+                    rph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 2 || warp == 3) {
+        // input prep: d' = sg * ((dr, di), (di, -dr)) per (k, c)
+        const float sg = pow2_scale(P.scales[5]);
+        for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
+            wait_slow(&rfull[r], rph);
+            uint8_t *in = in_base + r * IN_STAGE;
+            const float2 *d = reinterpret_cast<const float2 *>(in + OFF_D);
+            float4 *dp = reinterpret_cast<float4 *>(in + OFF_DP);
+#pragma unroll
+            for (int e = (warp - 2) * 32 + lane; e < 32 * CP; e += 64) {
+                const float2 v = d[e];
+                dp[e] = make_float4(sg * v.x, sg * v.y, sg * v.y, -sg * v.x);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dfull[r]);
+            if (++r == NR) {
+                r = 0;
+                rph ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // MMA issuer: three N-wide MMAs per K step into the one accumulator
+        const uint32_t idesc = idesc_f16(128, N);
+        int i = 0;
+        for (int ch = 0; ch < nchain; ++ch) {
+            wait_fast(acc_empty, (ch & 1) ^ 1);
+            tc_fence_after();
+            const int iend = min(nkb, i + chain);
+            for (int i0 = i; i < iend; ++i) {
+                const int sa = i % NA, sb = i % NB;
+                wait_fast(&gen[sa], (i / NA) & 1);
+                wait_fast(&bfull[sb], (i / NB) & 1);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + sb * BST);
+                const uint32_t a_hi = tmem + a_col0 + 64 * sa, a_lo = a_hi + 32;
+                if (elect_one()) {
+                    if (!(P.exp_flags & 2)) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t dbh = desc_sw128(st + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + N * 128 + kk * 32);
+                            const uint32_t acc = (i != i0) || (kk != 0);
+                            mma_f16_ts(tmem, a_hi + 8 * kk, dbh, idesc, acc);
+                            mma_f16_ts(tmem, a_hi + 8 * kk, dbl, idesc, 1);
+                            mma_f16_ts(tmem, a_lo + 8 * kk, dbh, idesc, 1);
+                        }
+                    }
+                    mma_commit(&bempty[sb]);
+                    mma_commit(&aempty[sa]);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) mma_commit(acc_full);
+            __syncwarp();
+        }
+    } else if (warp >= 4 && warp < 4 + GW) {
+        // generators: lane quarter q, row m = (x, c, part), 32 samples
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int j = m >> 1, part = m & 1;
+        const int xl = j / CP, c = j % CP;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
+            const int sa = i % NA;
+            wait_fast(&dfull[r], rph);
+            const uint8_t *in = in_base + r * IN_STAGE;
+            const float2 *p0s = reinterpret_cast<const float2 *>(in);
+            const float2 *dps = reinterpret_cast<const float2 *>(in + OFF_DP) + (c * 2 + part);
+            uint32_t hv[SPW], lv[SPW];
+            if (P.exp_flags & 1) {
+#pragma unroll
+                for (int k = 0; k < SPW; ++k) hv[k] = lv[k] = 0u;
+            } else
+#pragma unroll
+            for (int k = 0; k < SPW; ++k) {
+                const float2 p = p0s[k * XS + xl], u = dps[k * CP * 2];
+                const float e0 = fmaf(p.x, u.x, p.y * u.y);
+                const float e1 = fmaf(p.y, u.x, -(p.x * u.y));
+                const __half2 hh = __floats2half2_rn(e0, e1);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(e0 - hf.x, e1 - hf.y);
+                hv[k] = *reinterpret_cast<const uint32_t *>(&hh);
+                lv[k] = *reinterpret_cast<const uint32_t *>(&ll);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[r]);
+            if (++r == NR) {
+                r = 0;
+                rph ^= 1;
+            }
+            wait_fast(&aempty[sa], ((i / NA) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t col = lane_base + a_col0 + 64 * sa;
+            tmem_st32(col, hv);
+            tmem_st32(col + 32, lv);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gen[sa]);
+        }
+    }
+    float sum[128];  // epilogue warps: running sums of row m over y in [0, 128)
+    if (run && warp >= 4 + GW) {
+        const int q = warp & 3;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int y = 0; y < 128; ++y) sum[y] = 0.f;
+        const int nhi = (N - 128) / 8;  // 8-column chunks of y >= 128
+        for (int ch = 0; ch < nchain; ++ch) {
+            wait_slow(acc_full, ch & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int cb = 0; cb < 8; ++cb) {
+                uint32_t r[16];
+                tmem_ld16(lane_base + cb * 16, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int yy = 0; yy < 16; ++yy) sum[cb * 16 + yy] += __uint_as_float(r[yy]);
+            }
+            for (int cb = 0; cb < nhi; ++cb) {
+                uint32_t r[8], sv[8];
+                tmem_ld8(lane_base + 128 + cb * 8, r);
+                if (ch > 0) tmem_ld8(lane_base + s_col0 + cb * 8, sv);
+                tmem_ld_wait();
+                if (cb == nhi - 1) {  // accumulator fully read: let the MMA go on
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty);
+                }
+#pragma unroll
+                for (int yy = 0; yy < 8; ++yy)
+                    sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
+                                             __uint_as_float(r[yy]));
+                tmem_st8(lane_base + s_col0 + cb * 8, sv);
+            }
+            tmem_st_wait();
+        }
+    }
+    __syncthreads();  // all MMAs and TMA loads are done: the B ring is free
+    if (run && warp >= 4 + GW) {
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int y = 0; y < 128; ++y) sum_s[y * ADJ_SUM_LD + m] = sum[y];
+        tc_fence_after();
+        for (int cb = 0; cb < (N - 128) / 8; ++cb) {
+            uint32_t sv[8];
+            tmem_ld8(lane_base + s_col0 + cb * 8, sv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int yy = 0; yy < 8; ++yy)
+                sum_s[(128 + cb * 8 + yy) * ADJ_SUM_LD + m] = __uint_as_float(sv[yy]);
+        }
+    }
+    __syncthreads();
+    // coil combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y)
+    if (run) {
+        const float inv = 1.f / pow2_scale(P.scales[5]);
+        const int64_t nxy = (int64_t)P.a.nx * P.a.ny;
+        float2 *wbase = P.ws + ((int64_t)s_id * P.a.T + t) * nxy;
+        for (int idx = threadIdx.x; idx < N * XS; idx += ADJW_THREADS) {
+            const int e = idx % N, xq = idx / N;
+            const int y = nt * N + e;
+            const int xg = mt * XS + xq;
+            if (y >= P.a.ny || xg >= P.a.nx) continue;
+            const float *row = sum_s + e * ADJ_SUM_LD;
+            float ar = 0.f, ai = 0.f;
+#pragma unroll
+            for (int cc = 0; cc < CP; ++cc) {
+                if (cc < P.a.C) {
+                    const float re = row[2 * (xq * CP + cc)];
+                    const float im = row[2 * (xq * CP + cc) + 1];
+                    const float2 sv = __ldg(P.sens + (int64_t)cc * nxy + (int64_t)xg * P.a.ny + y);
+                    ar += sv.x * re + sv.y * im;
+                    ai += sv.x * im - sv.y * re;
+                }
+            }
+            wbase[(int64_t)xg * P.a.ny + y] = make_float2(ar * inv, ai * inv);
+        }
+    }
+    __syncthreads();
+    if (run) probe_exit(P.probe);
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace csr

@@ -47,9 +47,14 @@ constexpr int TC_FWD_THREADS = 192;   // TMA, MMA, 4 epilogue warps
 #define TC_CHAIN 24
 #endif
 constexpr int TC_MAX_CHAIN = TC_CHAIN;  // max k blocks (32 samples) per accumulation chain
-// coils a tensor-core plan holds (padded to CP = 4, 8, ..., 64: 64 / CP x
-// values per adjoint tile row block, >= 1); more go to the SIMT kernels
-constexpr int TC_MAX_COILS = 64;
+#ifndef TC_ADJW_CHAIN
+#define TC_ADJW_CHAIN 12  // the wide adjoint's chains (one accumulator, 3 MMAs per K step)
+#endif
+// coils a tensor-core plan holds (padded to CP = 4, 8, 16, 32: 64 / CP x
+// values per adjoint tile row block; the P0 input box of the adjoint needs
+// >= 2 of them, TMA boxes being multiples of 16 bytes); more go to the SIMT
+// kernels
+constexpr int TC_MAX_COILS = 32;
 
 struct TcPlan {
     bool enabled = false;
@@ -69,6 +74,10 @@ struct TcPlan {
     int fts_ctas = 1, fts_smem = 0, fts_pieces = 1;
     unsigned *ftick = nullptr;             // forward piece tickets [T * mt_f]
     int raw_bytes = 0, adj_stage = 0, adj_nraw = 4, fwd_smem = 0, adj_smem = 0;
+    int adj_chain = TC_MAX_CHAIN;
+    // wide adjoint (k_tc_adjoint_w, 128 < ny): N-row y tiles, stages, smem
+    bool adj_w = false;
+    int adjw_N = 128, adjw_nyt = 1, adjw_NA = 4, adjw_NB = 2, adjw_nraw = 2, adjw_smem = 0;
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
@@ -80,6 +89,7 @@ struct TcPlan {
     unsigned *tick = nullptr;
     CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
     CUtensorMap tm_xb256_hi, tm_xb256_lo;
+    CUtensorMap tm_gaw_hi, tm_gaw_lo;  // N-row boxes of ga (wide adjoint)
 };
 
 // last CUDA error string of a failed tensor-core launch (for csr_last_error)

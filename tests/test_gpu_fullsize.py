@@ -92,5 +92,12 @@ def test_truncated_admm_vs_cpu_reference(cuda, cfg):
     assert [r["cg_iterations"] for r in rep.iterations] == [5] * iters
     assert err <= IMG_TOL
     assert max(per_frame) <= IMG_TOL
-    # ADMM relative changes (solver.py:149-155) track the reference's
-    np.testing.assert_allclose([r["alpha"] for r in rep.iterations], g["alpha"], rtol=1e-3)
+    # ADMM relative changes (solver.py:149-155) track the reference's while
+    # above the single-precision floor (the iterate stops moving by the third
+    # iteration: ||rho_k - rho_k-1||^2 / ||rho_k-1||^2 ~ 1e-19 in f64 and
+    # ~1e-14 = fp32 rounding squared here)
+    for got_a, ref_a in zip([r["alpha"] for r in rep.iterations], g["alpha"]):
+        if ref_a > 1e-10:
+            assert abs(got_a - ref_a) <= 1e-3 * ref_a, (got_a, ref_a)
+        else:
+            assert got_a <= 1e-11, (got_a, ref_a)

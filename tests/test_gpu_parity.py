@@ -77,11 +77,11 @@ def test_operator_random_shapes_vs_direct_sum(cuda):
     (32, 200, 16, 1500),   # ny % 128 = 72, 16 coils
     (96, 136, 5, 2048),    # ny % 128 = 8: a mostly empty last tile
     (64, 64, 32, 3000),    # 32 coils: CP = 32 tensor-core tiles (2 x per adjoint row block)
-    (40, 96, 48, 2000),    # 48 coils padded to CP = 64 (one x per adjoint row block)
-    (24, 20, 66, 700),     # > 64 coils: the SIMT kernels
+    (40, 96, 48, 2000),    # > 32 coils: the SIMT kernels
+    (24, 20, 66, 700),     # (and 66 coils)
 ])
 def test_operator_tile_shapes_vs_oracle(cuda, nx, ny, nc, m):
-    op_path = "simt" if nc > 64 else "tcgen05"
+    op_path = "simt" if nc > 32 else "tcgen05"
     # ragged adjoint y tiles (128 pixel rows, zero-padded factor rows) and
     # forward K padding; both operators vs the f64 separable restatement
     # (kernels.py:71-88)
@@ -535,7 +535,7 @@ def test_soft_threshold_is_the_prox(cuda):
     (1, 1, 24, 3, 60),      # degenerate 1 x ny image
     (2, 12, 10, 5, 130),    # 2-D+t, two frames
     (1, 40, 36, 32, 900),   # 32 coils (CP = 32 tensor-core path)
-    (1, 20, 18, 66, 300),   # 66 coils: the SIMT path through the native loop
+    (1, 20, 18, 40, 300),   # 40 coils: the SIMT path through the native loop
 ])
 def test_admm_shapes_vs_oracle(cuda, T, nx, ny, C, m):
     # the native loop (head, forward, adjoint, tail, post) on ragged / extreme

@@ -71,7 +71,9 @@ def test_reference_admm_on_b200(ref):
     from csrecon.acquisition import KSpaceDataset, SensitivityMaps, Trajectory
     from csrecon.solver import ReconParams, admm_reconstruct, adjoint_reconstruct
     g = golden("admm_small.npz")
-    lam, beta, rtol, na, atol, ncg = g["fixed_params"]
+    # Python floats, as the fixture's own run used (numpy float64 parameters
+    # would promote the reference's single-precision vectors to complex128)
+    lam, beta, rtol, na, atol, ncg = (float(v) for v in g["fixed_params"])
     params = ReconParams(lam=lam, beta=beta, admm_rtol=rtol, admm_max_iters=int(na),
                          cg_atol=atol, cg_max_iters=int(ncg))
     ds = KSpaceDataset(g["data"], Trajectory(g["coords"], g["coords"].shape[0], 1))

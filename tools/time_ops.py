@@ -6,7 +6,8 @@ import paper_2006_14080_b200 as P
 from paper_2006_14080_b200 import _native
 from harness.configs import make_problem
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-prob = make_problem(cfg)
+prob = make_problem(cfg, encoder=(lambda img, s, k: np.zeros((k.shape[0], s.shape[0])))
+                    if cfg >= 2 else None)
 op = P.DftOperator.build(prob.coords, P.ImageGrid(prob.nx, prob.ny), prob.sens, n_frames=prob.n_frames)
 dev = op.device
 x = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(prob.truth, op.image_shape).astype(np.complex64))).to(dev)
@@ -29,5 +30,5 @@ for name in ("forward", "adjoint"):
 import ctypes
 fm, am, fn, an = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
 _native.call("csr_plan_kernel_times", op.plan, ctypes.byref(fm), ctypes.byref(am), ctypes.byref(fn), ctypes.byref(an))
-print(f"cfg {cfg} exp={os.environ.get('CSR_EXP','0')} split={op.info()['split_k']} fwd {res['forward']:.1f} us adj {res['adjoint']:.1f} us"
+print(f"cfg {cfg} variant={os.environ.get('CSR_VARIANT','product')} narrow={os.environ.get('CSR_ADJ_NARROW','0')} exp={os.environ.get('CSR_EXP','0')} split={op.info()['split_k']} fwd {res['forward']:.1f} us adj {res['adjoint']:.1f} us"
       f" | kernels fwd {fm.value*1e3:.1f} adj {am.value*1e3:.1f} us", flush=True)
