@@ -107,8 +107,9 @@ inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes, int bl
 struct AdjGeom {
     bool wide = false;
     int N = 128, nyt = 1, NA = 4, NB = 0, chain = TC_MAX_CHAIN, blk_cycles = 768;
+    int CL = 1;  // wide kernel: CTA pairs along x sharing B by TMA multicast
 };
-inline AdjGeom tc_adj_geom(int ny, int Cp) {
+inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     AdjGeom g;
     g.nyt = (ny + 127) / 128;
     if (ny <= 128 || Cp > 16 || dbg_env("CSR_ADJ_NARROW")) return g;
@@ -117,14 +118,21 @@ inline AdjGeom tc_adj_geom(int ny, int Cp) {
     g.N = ((ny + g.nyt - 1) / g.nyt + 15) / 16 * 16;
     // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128)
     g.NA = std::min(4, (512 - g.N - (g.N - 128)) / 64);
-    // B ring: enough stages to hold the combine's sums [N][ADJ_SUM_LD] afterwards
-    const int bst = adjw_b_stage(g.N);
-    g.NB = std::max(2, (g.N * ADJ_SUM_LD * 4 + bst - 1) / bst);
+    // B ring: two stages (the MMAs take ~1.3 us per K block, an L2-hit TMA
+    // refill ~1 us); the rest of shared memory deepens the input ring, whose
+    // TMA -> prep -> generator -> release round trip bounds the kernel with
+    // two stages (measured: the skeleton without math or MMAs ran at 0.66 us
+    // per K block with NB = 3, NR = 2).  The combine's sums reuse both rings.
+    g.NB = 2;
+    if (const char *e = dbg_env("CSR_ADJW_NB")) g.NB = std::max(2, std::min(4, atoi(e)));
     // three N-wide MMAs per K step truncate into one fp32 accumulator:
     // shorter chains than the two-accumulator kernel
     g.chain = TC_ADJW_CHAIN;
     if (const char *e = dbg_env("CSR_ADJW_CHAIN")) g.chain = std::max(1, atoi(e));
     g.blk_cycles = 4 * 3 * (g.N / 2 + 32);
+    // pairs of x tiles multicast the B tiles (half the rows each: a multiple of 8)
+    g.CL = (mt_a % 2 == 0 && (g.N / 2) % 8 == 0) ? 2 : 1;
+    if (const char *e = dbg_env("CSR_ADJW_CL")) g.CL = (atoi(e) == 2 && mt_a % 2 == 0) ? 2 : 1;
     return g;
 }
 
@@ -196,6 +204,9 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // (<= 16 coils: the persistent form's 576-thread CTA keeps CP complex
     // accumulators per epilogue thread in registers)
     tc.fwd_ts = tc.Kf <= 256 && Cp <= 16 && !dbg_env("CSR_FWD_SS") && chunk == 0;
+    // SS form: pairs of sample tiles of one frame multicast the image operand
+    tc.fwd_CL = (tc.mt_f % 2 == 0) ? 2 : 1;
+    if (const char *e = dbg_env("CSR_FWD_CL")) tc.fwd_CL = (atoi(e) == 2 && tc.mt_f % 2 == 0) ? 2 : 1;
     // PS form of the persistent forward (A staged from shared memory next
     // to B, two accumulators so the drain overlaps the next unit's MMAs):
     // measured faster than A in tensor memory (config 1 39.4 vs 41.8 us,
@@ -232,8 +243,9 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // adjoint split-K
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
-    const AdjGeom ag = tc_adj_geom(ny, Cp);
+    const AdjGeom ag = tc_adj_geom(ny, Cp, tc.mt_a);
     tc.adj_w = ag.wide;
+    tc.adjw_CL = ag.CL;
     tc.adjw_N = ag.N;
     tc.adjw_nyt = ag.nyt;
     tc.adjw_NA = ag.NA;
@@ -264,7 +276,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         const int fixed = tc.adjw_NB * adjw_b_stage(tc.adjw_N) + 1024 + 512;
         tc.adjw_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
         tc.adjw_smem = fixed + tc.adjw_nraw * tc.adj_stage;
-        if (tc.adjw_nraw < 2) tc.adj_w = false;  // keep the narrow kernel
+        // the combine's sums [N][ADJ_SUM_LD] floats over the B and input rings
+        const int rings = fixed - 1536 + tc.adjw_nraw * tc.adj_stage;
+        if (tc.adjw_nraw < 2 || tc.adjw_N * ADJ_SUM_LD * 4 > rings)
+            tc.adj_w = false;  // keep the narrow kernel
     }
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
@@ -315,24 +330,35 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
               tmap_f16_2d(&tc.tm_fa_lo, tc.fa_lo, tc.Kf, (uint64_t)T * tc.Mk, TC_BM) &&
               tmap_f16_2d(&tc.tm_xb_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
               tmap_f16_2d(&tc.tm_xb_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN) &&
+              tmap_f16_2d(&tc.tm_xb128_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, TC_BN / 2) &&
+              tmap_f16_2d(&tc.tm_xb128_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, TC_BN / 2) &&
               tmap_f16_2d(&tc.tm_xb256_hi, tc.xb_hi, tc.Kf, (uint64_t)T * tc.Nf, 256) &&
               tmap_f16_2d(&tc.tm_xb256_lo, tc.xb_lo, tc.Kf, (uint64_t)T * tc.Nf, 256) &&
               tmap_f16_2d(&tc.tm_ga_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               tmap_f16_2d(&tc.tm_ga_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, 128) &&
               (!tc.adj_w ||
-               (tmap_f16_2d(&tc.tm_gaw_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA, tc.adjw_N) &&
-                tmap_f16_2d(&tc.tm_gaw_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA, tc.adjw_N))) &&
+               (tmap_f16_2d(&tc.tm_gaw_hi, tc.ga_hi, 2 * tc.Mk, (uint64_t)T * tc.nyA,
+                            tc.adjw_N / tc.adjw_CL) &&
+                tmap_f16_2d(&tc.tm_gaw_lo, tc.ga_lo, 2 * tc.Mk, (uint64_t)T * tc.nyA,
+                            tc.adjw_N / tc.adjw_CL))) &&
               tmap_c64_3d(&tc.tm_p0, tc.p0p, tc.nxp, tc.Mk, T, 64 / Cp, 32) &&
               tmap_c64_3d(&tc.tm_kd, tc.kdi, Cp, tc.Mk, T, Cp, 32);
     if (!ok) return 0;  // descriptor encode unavailable: SIMT path
     switch (Cp) {
-        case 4: set_smem(k_tc_forward<4>, tc.fwd_smem); set_smem(k_tc_adjoint<4>, tc.adj_smem);
-                set_smem(k_tc_adjoint_w<4>, tc.adjw_smem); break;
-        case 8: set_smem(k_tc_forward<8>, tc.fwd_smem); set_smem(k_tc_adjoint<8>, tc.adj_smem);
-                set_smem(k_tc_adjoint_w<8>, tc.adjw_smem); break;
-        case 16: set_smem(k_tc_forward<16>, tc.fwd_smem); set_smem(k_tc_adjoint<16>, tc.adj_smem);
-                 set_smem(k_tc_adjoint_w<16>, tc.adjw_smem); break;
-        case 32: set_smem(k_tc_forward<32>, tc.fwd_smem); set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
+        case 4: set_smem(k_tc_forward<4, 1>, tc.fwd_smem); set_smem(k_tc_forward<4, 2>, tc.fwd_smem);
+                set_smem(k_tc_adjoint<4>, tc.adj_smem);
+                set_smem(k_tc_adjoint_w<4, 1>, tc.adjw_smem); set_smem(k_tc_adjoint_w<4, 2>, tc.adjw_smem);
+                break;
+        case 8: set_smem(k_tc_forward<8, 1>, tc.fwd_smem); set_smem(k_tc_forward<8, 2>, tc.fwd_smem);
+                set_smem(k_tc_adjoint<8>, tc.adj_smem);
+                set_smem(k_tc_adjoint_w<8, 1>, tc.adjw_smem); set_smem(k_tc_adjoint_w<8, 2>, tc.adjw_smem);
+                break;
+        case 16: set_smem(k_tc_forward<16, 1>, tc.fwd_smem); set_smem(k_tc_forward<16, 2>, tc.fwd_smem);
+                 set_smem(k_tc_adjoint<16>, tc.adj_smem);
+                 set_smem(k_tc_adjoint_w<16, 1>, tc.adjw_smem); set_smem(k_tc_adjoint_w<16, 2>, tc.adjw_smem);
+                 break;
+        case 32: set_smem(k_tc_forward<32, 1>, tc.fwd_smem); set_smem(k_tc_forward<32, 2>, tc.fwd_smem);
+                 set_smem(k_tc_adjoint<32>, tc.adj_smem); break;
         default: break;
     }
     if (tc_alloc(allocs, &p, PROBE_SLOTS * 4 * sizeof(unsigned long long), ws_bytes, st)) return 2;
@@ -436,10 +462,16 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.exp_flags = tc.fexp;
         dim3 grid((unsigned)(tc.T * tc.mt_f), (unsigned)G);
         switch (tc.Cp) {
-            case 4: launch(k_tc_forward<4>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            case 8: launch(k_tc_forward<8>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            case 16: launch(k_tc_forward<16>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
-            default: launch(k_tc_forward<32>, grid, TC_FWD_THREADS, tc.fwd_smem, st, tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P); break;
+#define FWD_LAUNCH(CPV)                                                                         \
+    (tc.fwd_CL > 1 ? launch_cl(k_tc_forward<CPV, 2>, grid, TC_FWD_THREADS, tc.fwd_smem, st, 2,    \
+                               tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb128_hi, tc.tm_xb128_lo, P)       \
+                   : launch(k_tc_forward<CPV, 1>, grid, TC_FWD_THREADS, tc.fwd_smem, st,          \
+                            tc.tm_fa_hi, tc.tm_fa_lo, tc.tm_xb_hi, tc.tm_xb_lo, P))
+            case 4: FWD_LAUNCH(4); break;
+            case 8: FWD_LAUNCH(8); break;
+            case 16: FWD_LAUNCH(16); break;
+            default: FWD_LAUNCH(32); break;
+#undef FWD_LAUNCH
         }
     }
     if (!direct) {
@@ -506,11 +538,27 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
         P.scales = tc.scales;
         P.gate = gate;
         cfg.gridDim = dim3((unsigned)tc.mt_a, (unsigned)tc.adjw_nyt, (unsigned)(tc.T * tc.split));
-        switch (tc.Cp) {
-            case 4: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<4>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
-            case 8: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<8>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
-            default: e = cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<16>, tc.tm_gaw_hi, tc.tm_gaw_lo, tc.tm_p0, tc.tm_kd, P); break;
+        cudaLaunchAttribute wattr[2];
+        wattr[0] = attr[0];
+        wattr[1].id = cudaLaunchAttributeClusterDimension;
+        wattr[1].val.clusterDim.x = (unsigned)tc.adjw_CL;
+        wattr[1].val.clusterDim.y = 1;
+        wattr[1].val.clusterDim.z = 1;
+        if (tc.adjw_CL > 1) {
+            cfg.attrs = wattr + (pdl_enabled() ? 0 : 1);
+            cfg.numAttrs = pdl_enabled() ? 2 : 1;
         }
+#define ADJW_LAUNCH(CPV)                                                                        \
+    (tc.adjw_CL > 1 ? cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<CPV, 2>, tc.tm_gaw_hi, tc.tm_gaw_lo, \
+                                         tc.tm_p0, tc.tm_kd, P)                                 \
+                    : cudaLaunchKernelEx(&cfg, k_tc_adjoint_w<CPV, 1>, tc.tm_gaw_hi, tc.tm_gaw_lo, \
+                                         tc.tm_p0, tc.tm_kd, P))
+        switch (tc.Cp) {
+            case 4: e = ADJW_LAUNCH(4); break;
+            case 8: e = ADJW_LAUNCH(8); break;
+            default: e = ADJW_LAUNCH(16); break;
+        }
+#undef ADJW_LAUNCH
     } else {
         AdjParams P;
         P.a = a;

@@ -22,6 +22,13 @@
 // Roles (12 warps): 0 lane 0 B-ring TMA, lane 1 input-ring TMA; 1 MMA
 // issuer (elected lane); 2-3 input prep (d'); 4-7 generators (one per TMEM
 // lane quarter, 32 samples each); 8-11 epilogue.
+//
+// CL = 2: CTA pairs along x (a cluster of two x tiles of the same frame,
+// y tile and k range) share the static B tiles: each CTA fetches half of
+// the N rows and multicasts them to both, so the L2 -> SM traffic of the
+// dominant operand halves.  A B stage is refilled only after the MMAs of
+// BOTH CTAs released it (the MMA commit is multicast to the pair's
+// bempty barriers, which count CL arrivals).
 #pragma once
 
 #include "tc_adjoint.cuh"
@@ -49,7 +56,7 @@ struct AdjWParams {
 // barriers; the coil-combine sums [N][ADJ_SUM_LD] floats reuse the B ring
 __host__ __device__ constexpr int adjw_b_stage(int N) { return 2 * N * 128; }
 
-template <int CP>
+template <int CP, int CL>
 __global__ void __launch_bounds__(ADJW_THREADS, 1)
     k_tc_adjoint_w(const __grid_constant__ CUtensorMap tmB_hi,
                    const __grid_constant__ CUtensorMap tmB_lo,
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         tma_prefetch(&tmKd);
         for (int s = 0; s < NB; ++s) {
             mbar_init(&bfull[s], 1);
-            mbar_init(&bempty[s], 1);
+            mbar_init(&bempty[s], CL);
         }
         for (int s = 0; s < NA; ++s) {
             mbar_init(&gen[s], GW);
@@ -113,21 +120,29 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
+    if (CL > 1) cluster_sync();  // the peer's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+    const int hrows = N / CL;  // B rows this CTA fetches (and multicasts)
+    auto load_b = [&](uint8_t *st, uint64_t *bar, int kb, int brow) {
+        mbar_arrive_expect_tx(bar, BST);
+        if (CL == 1) {
+            tma_load_2d(st, &tmB_hi, bar, kb * 64, brow);
+            tma_load_2d(st + N * 128, &tmB_lo, bar, kb * 64, brow);
+        } else {
+            const int o = (int)crank * hrows;
+            tma_load_2d_mc(st + o * 128, &tmB_hi, bar, kb * 64, brow + o, (1u << CL) - 1);
+            tma_load_2d_mc(st + (N + o) * 128, &tmB_lo, bar, kb * 64, brow + o, (1u << CL) - 1);
+        }
+    };
     const uint32_t a_col0 = (uint32_t)N;                 // A stages
     const uint32_t s_col0 = (uint32_t)(N + 64 * NA);     // running sums of cols >= 128
     // the first B stages (static factor) before the programmatic wait
     const int pre = min(nkb, NB);
     const int brow = t * P.a.nyA + nt * N;
-    if (warp == 0 && lane == 0) {
-        for (int i = 0; i < pre; ++i) {
-            uint8_t *st = smem + i * BST;
-            mbar_arrive_expect_tx(&bfull[i], BST);
-            tma_load_2d(st, &tmB_hi, &bfull[i], (kb0 + i) * 64, brow);
-            tma_load_2d(st + N * 128, &tmB_lo, &bfull[i], (kb0 + i) * 64, brow);
-        }
-    }
+    if (warp == 0 && lane == 0)
+        for (int i = 0; i < pre; ++i) load_b(smem + i * BST, &bfull[i], kb0 + i, brow);
     pdl_wait();
     const bool run = !P.gate || *P.gate;
     if (run) probe_enter(P.probe);
@@ -141,10 +156,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                 const int kb = kb0 + i;
                 const int s = i % NB;
                 wait_slow(&bempty[s], ((i / NB) & 1) ^ 1);
-                uint8_t *st = smem + s * BST;
-                mbar_arrive_expect_tx(&bfull[s], BST);
-                tma_load_2d(st, &tmB_hi, &bfull[s], kb * 64, brow);
-                tma_load_2d(st + N * 128, &tmB_lo, &bfull[s], kb * 64, brow);
+                load_b(smem + s * BST, &bfull[s], kb, brow);
             }
         } else if (lane == 1) {
             const uint32_t tx = P.raw_bytes;
@@ -208,7 +220,8 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                             mma_f16_ts(tmem, a_lo + 8 * kk, dbh, idesc, 1);
                         }
                     }
-                    mma_commit(&bempty[sb]);
+                    if (CL > 1) mma_commit_mc(&bempty[sb], (uint16_t)((1u << CL) - 1));
+                    else mma_commit(&bempty[sb]);
                     mma_commit(&aempty[sa]);
                 }
                 __syncwarp();
@@ -344,6 +357,9 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     }
     __syncthreads();
     if (run) probe_exit(P.probe);
+    // no CTA of a pair leaves while the peer's MMA commits may still
+    // arrive on its barriers
+    if (CL > 1) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);

@@ -78,6 +78,7 @@ struct TcPlan {
     // wide adjoint (k_tc_adjoint_w, 128 < ny): N-row y tiles, stages, smem
     bool adj_w = false;
     int adjw_N = 128, adjw_nyt = 1, adjw_NA = 4, adjw_NB = 2, adjw_nraw = 2, adjw_smem = 0;
+    int adjw_CL = 1;  // CTA-pair clusters multicasting B
     // operands
     __half *fa_hi = nullptr, *fa_lo = nullptr, *ga_hi = nullptr, *ga_lo = nullptr;
     __half *xb_hi = nullptr, *xb_lo = nullptr;
@@ -90,6 +91,8 @@ struct TcPlan {
     CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
     CUtensorMap tm_xb256_hi, tm_xb256_lo;
     CUtensorMap tm_gaw_hi, tm_gaw_lo;  // N-row boxes of ga (wide adjoint)
+    CUtensorMap tm_xb128_hi, tm_xb128_lo;  // half-tile boxes of xb (multicast pairs)
+    int fwd_CL = 1;  // SS forward: CTA-pair clusters multicasting the image operand
 };
 
 // last CUDA error string of a failed tensor-core launch (for csr_last_error)

@@ -32,7 +32,13 @@ struct FwdParams {
 };
 
 
-template <int CP>
+// CL = 2: pairs of consecutive sample tiles of the same frame (a cluster
+// along x) share the image operand B: each CTA fetches half of the 256 B
+// rows of every K block and multicasts them to both CTAs, so the L2 -> SM
+// traffic per K block drops from 96 to 64 KiB per CTA.  A stage is
+// refilled only after the MMAs of both CTAs released it (multicast commit
+// onto the pair's `empty` barriers, which count CL arrivals).
+template <int CP, int CL>
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     k_tc_forward(const __grid_constant__ CUtensorMap tmA_hi,
                  const __grid_constant__ CUtensorMap tmA_lo,
@@ -40,6 +46,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                  const __grid_constant__ CUtensorMap tmB_lo, FwdParams P) {
     pdl_enter();
     using namespace sm100;
+    // (the gate is uniform over the grid, so a pair leaves together)
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
     extern __shared__ uint8_t smem_raw[];
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
         tma_prefetch(&tmB_lo);
         for (int s = 0; s < TC_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CL);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -74,8 +81,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
+    if (CL > 1) cluster_sync();  // the peer's barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -94,8 +103,17 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                     mbar_arrive_expect_tx(&full[s], TC_FWD_OPS);
                     tma_load_2d(st, &tmA_hi, &full[s], kb * 64, mtile * TC_BM);
                     tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, mtile * TC_BM);
-                    tma_load_2d(st + 2 * TC_A_TILE, &tmB_hi, &full[s], kb * 64, brow);
-                    tma_load_2d(st + 2 * TC_A_TILE + TC_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                    if (CL == 1) {
+                        tma_load_2d(st + 2 * TC_A_TILE, &tmB_hi, &full[s], kb * 64, brow);
+                        tma_load_2d(st + 2 * TC_A_TILE + TC_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
+                    } else {
+                        const int o = (int)crank * (TC_BN / CL);
+                        const uint16_t mask = (uint16_t)((1u << CL) - 1);
+                        tma_load_2d_mc(st + 2 * TC_A_TILE + o * 128, &tmB_hi, &full[s], kb * 64,
+                                       brow + o, mask);
+                        tma_load_2d_mc(st + 2 * TC_A_TILE + TC_B_TILE + o * 128, &tmB_lo, &full[s],
+                                       kb * 64, brow + o, mask);
+                    }
                 }
             }
         }
@@ -131,7 +149,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                             mma_f16_lastuse(dcol, dah, dbl, idesc, 1);
                             mma_f16(dcol, dal, dbh, idesc, 1);
                         }
-                        mma_commit(&empty[s]);
+                        if (CL > 1) mma_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1));
+                        else mma_commit(&empty[s]);
                     }
                     if (FWD_SS_ELECT) __syncwarp();
                 }
@@ -203,6 +222,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     }
     __syncthreads();
     probe_exit(P.probe);
+    // no CTA of a pair leaves while the peer's MMA commits may still arrive
+    if (CL > 1) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
