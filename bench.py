@@ -47,8 +47,10 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 METRIC = "ADMM iters/s"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of each NUDFT GEMM
 # (the roofline reports the dominant one), from one `ncu --set full`
-# capture (profiles/r01d_ncu_gemm.txt; cold cache: the factors come from HBM)
-TRAFFIC = {1: {"forward": 35694336 + 256, "adjoint": 35693824}}
+# capture each (cold cache: the factors come from HBM): config 1
+# profiles/r01d_ncu_gemm.txt, config 4 profiles/r02i_ncu_gemm_c4.txt
+TRAFFIC = {1: {"forward": 35694336 + 256, "adjoint": 35693824},
+           4: {"forward": 4466634000 + 90215936, "adjoint": 3733654000 + 44685056}}
 
 
 def peaks():

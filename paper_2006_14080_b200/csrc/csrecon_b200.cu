@@ -99,6 +99,9 @@ struct csr_plan {
     // frame sharding (CSR_PLAN_FRAME_SHARD): halo frames and scalar slots
     bool frame_mode = false;
     float2 *hprev = nullptr, *hnext = nullptr, *sfirst = nullptr, *slast = nullptr;
+    float2 *hprev_own = nullptr, *hnext_own = nullptr;  // the no-comm halo buffers
+    float2 *hsend = nullptr, *hgath = nullptr;  // with a comm: [first|last], gathered pairs
+    size_t hgath_ranks = 0;
     double *loc = nullptr;
     double *mpart = nullptr;  // grid-max partials of the d producers
     double *tail_part = nullptr;  // fused CG head / tail: [8][<= 1024 blocks] partials
@@ -275,26 +278,27 @@ bool multi_rank_scalars(const csr_plan *p) { return p->frame_mode && p->comm; }
 
 // Ring halo exchange of one frame each way: hprev <- previous rank's `last`,
 // hnext <- next rank's `first` (ranks in frame order, circular like the
-// temporal difference).  One rank: local copies, communicator or not — NCCL
-// send/recv to self inside a captured graph never completes (measured with
-// NCCL 2.28.9 on B200, tools/nccl_self_probe.cu: eager self send/recv works,
-// the same group captured and replayed hangs), so only P > 1 uses NCCL here.
+// temporal difference).  Without a communicator: local copies.  With one,
+// every rank contributes its [first | last] pair to an NCCL all-gather and
+// hprev / hnext point at the neighbours' slots of the gathered pairs
+// (csr_plan_set_comm), so the exchange is one collective inside the
+// captured graph, at any rank count.  (A ring of ncclSend/ncclRecv is the
+// leaner pattern at P > 2, but NCCL send/recv to self inside a captured
+// graph never completes — measured with NCCL 2.28.9 on the B200,
+// tools/nccl_self_probe.cu — so the one-rank path could not exercise it;
+// the boundary frames are 0.5 MB each at config 4, the all-gather of 2 P of
+// them per CG iteration is noise next to the GEMMs.)
 int halo_exchange(csr_plan *p, const float2 *first, const float2 *last, cudaStream_t st) {
     const size_t nb = (size_t)p->nx * p->ny * sizeof(float2);
-    const int P = nranks(p);
-    if (P == 1) {
+    if (!p->comm) {
         CU(cudaMemcpyAsync(p->hprev, last, nb, cudaMemcpyDeviceToDevice, st));
         CU(cudaMemcpyAsync(p->hnext, first, nb, cudaMemcpyDeviceToDevice, st));
         return CSR_OK;
     }
-    const int r = p->comm->rank, nxt = (r + 1) % P, prv = (r + P - 1) % P;
-    const size_t nf = 2 * (size_t)p->nx * p->ny;
-    NC(ncclGroupStart());
-    NC(ncclSend(last, nf, ncclFloat, nxt, p->comm->comm, st));
-    NC(ncclRecv(p->hprev, nf, ncclFloat, prv, p->comm->comm, st));
-    NC(ncclSend(first, nf, ncclFloat, prv, p->comm->comm, st));
-    NC(ncclRecv(p->hnext, nf, ncclFloat, nxt, p->comm->comm, st));
-    NC(ncclGroupEnd());
+    const size_t nf = (size_t)p->nx * p->ny;
+    CU(cudaMemcpyAsync(p->hsend, first, nb, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(p->hsend + nf, last, nb, cudaMemcpyDeviceToDevice, st));
+    NC(ncclAllGather(p->hsend, p->hgath, 4 * nf, ncclFloat, p->comm->comm, st));
     return CSR_OK;
 }
 
@@ -683,6 +687,8 @@ int plan_create(const csr_plan_desc *desc, const FactorSource &fs, csr_plan **ou
     if (p->frame_mode) {
         if ((rc = dalloc(p, &p->hprev, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
         if ((rc = dalloc(p, &p->hnext, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
+        p->hprev_own = p->hprev;
+        p->hnext_own = p->hnext;
         if ((rc = dalloc(p, &p->sfirst, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
         if ((rc = dalloc(p, &p->slast, (size_t)nxy, &p->ws_bytes))) return cleanup(rc);
     }
@@ -1238,6 +1244,24 @@ int csr_plan_set_comm(csr_plan *p, csr_comm *c) {
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
+    }
+    if (p->frame_mode) {
+        // halo pairs all-gathered: this rank's neighbours' slots (circular)
+        CU(cudaSetDevice(p->dev));
+        if (c) {
+            const size_t nf = (size_t)p->nx * p->ny;
+            if (!p->hgath || p->hgath_ranks != (size_t)c->nranks) {
+                TRY(dalloc(p, &p->hsend, 2 * nf, &p->ws_bytes));
+                TRY(dalloc(p, &p->hgath, (size_t)c->nranks * 2 * nf, &p->ws_bytes));
+                p->hgath_ranks = (size_t)c->nranks;
+            }
+            const int P = c->nranks, r = c->rank;
+            p->hprev = p->hgath + (size_t)((r + P - 1) % P) * 2 * nf + nf;  // prev's last
+            p->hnext = p->hgath + (size_t)((r + 1) % P) * 2 * nf;           // next's first
+        } else {
+            p->hprev = p->hprev_own;
+            p->hnext = p->hnext_own;
+        }
     }
     if (p->ordered) {
         CU(cudaSetDevice(p->dev));

@@ -1,7 +1,7 @@
 """World-size-2 tests of the multi-GPU decomposition on CPU (gloo).
 
 The device loop shards coils (static problems: one image allreduce per CG
-iteration) or frames (2-D+t: ring halo exchange for the temporal
+iteration) or frames (2-D+t: halo exchange (all-gather of boundary frames) for the temporal
 differences, allreduced CG/ADMM scalars).  These tests run the same
 decomposition with the f64 oracle as the per-rank compute stand-in and gloo
 as the interconnect, and check it reproduces the unsharded solve; they also
@@ -56,17 +56,17 @@ def _allreduce(arr):
 
 
 def _ring_exchange(first, last, rank, world):
-    """hprev <- previous rank's last frame, hnext <- next rank's first frame
-    (the device loop's halo_exchange)."""
-    nxt, prv = (rank + 1) % world, (rank - 1) % world
-    send_l = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(last))).clone()
-    send_f = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(first))).clone()
-    recv_p, recv_n = torch.empty_like(send_l), torch.empty_like(send_f)
-    ops = [dist.P2POp(dist.isend, send_l, nxt), dist.P2POp(dist.irecv, recv_p, prv),
-           dist.P2POp(dist.isend, send_f, prv), dist.P2POp(dist.irecv, recv_n, nxt)]
-    for r in dist.batch_isend_irecv(ops):
-        r.wait()
-    return torch.view_as_complex(recv_p).numpy(), torch.view_as_complex(recv_n).numpy()
+    """hprev <- previous rank's last frame, hnext <- next rank's first frame,
+    as the device loop's halo_exchange does it: every rank contributes its
+    [first | last] pair to one all-gather and reads its neighbours' slots
+    (csrecon_b200.cu halo_exchange / csr_plan_set_comm)."""
+    pair = torch.view_as_real(torch.from_numpy(np.ascontiguousarray(
+        np.stack([first, last])))).clone()
+    gathered = [torch.empty_like(pair) for _ in range(world)]
+    dist.all_gather(gathered, pair)
+    prev = torch.view_as_complex(gathered[(rank - 1) % world][1].contiguous()).numpy()
+    nxt = torch.view_as_complex(gathered[(rank + 1) % world][0].contiguous()).numpy()
+    return prev, nxt
 
 
 def _theta_h(v, prev):

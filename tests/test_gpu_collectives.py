@@ -5,12 +5,13 @@ for any rank count (include/csrecon_b200.h): ``collective="nccl"`` gives a
 one-rank NCCL communicator, so the image allreduce (coil / plain sample
 split, sharding.py:211-250, solver.py:136), the chunk all-gather and the
 k-space max-allreduce (order-stable sample split, sharding.py:173-208), and
-the fp64 scalar allreduces of the frame split all execute through NCCL
-inside the captured iteration graph.  The frame split's ring halo uses NCCL
-send/recv only between different ranks: at one rank it is a local copy,
-because NCCL send/recv to self inside a captured graph never completes
-(tools/nccl_self_probe.cu, measured on the B200 with NCCL 2.28.9).  Each run is
-compared with the plain single-GPU run of the same problem.
+the frame split's halo all-gather and fp64 scalar allreduces all execute
+through NCCL inside the captured iteration graph.  (The halo is an
+all-gather of every rank's [first | last] frames rather than a ring of
+send/recv: NCCL send/recv to self inside a captured graph never completes,
+tools/nccl_self_probe.cu, measured on the B200 with NCCL 2.28.9, so only a
+collective lets the one-rank run take the same path as P ranks.)  Each run
+is compared with the plain single-GPU run of the same problem.
 """
 
 import numpy as np
@@ -65,9 +66,9 @@ def test_ordered_sample_path_is_bitwise(cuda):
 
 
 def test_frame_path_halo_and_scalar_allreduce(cuda):
-    # 2-D+t frame split: CG / ADMM scalars as fp64 NCCL sums before the
-    # device-side finalize (multi-rank scalar protocol), halo frames copied
-    # locally at one rank; against the plain run and the f64 restatement
+    # 2-D+t frame split: halo frames through the NCCL all-gather of the
+    # ranks' boundary pairs, CG / ADMM scalars as fp64 NCCL sums before the
+    # device-side finalize; against the plain run and the f64 restatement
     rng = np.random.default_rng(9)
     T, nx, ny, C, m = 3, 20, 16, 3, 250
     coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
