@@ -473,7 +473,8 @@ def run_ours(args, cfg, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         arm = CpuArm(prob)
         arm.seconds(1)  # numba JIT warm-up
-        n_cpu = 2 if cfg != 1 else 8
+        t1 = arm.seconds(1)
+        n_cpu = int(min(50, max(2, round(15.0 / max(t1, 1e-3)))))  # ~15 s of CPU work
         rate, dt = arm.rate(n_cpu)
         out["cpu_baseline"] = {"value": rate, "unit": "iter/s", "cores": arm.cores,
                                "kind": arm.kind,
