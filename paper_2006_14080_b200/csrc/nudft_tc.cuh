@@ -115,7 +115,9 @@ inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     if (ny <= 128 || Cp > 16 || dbg_env("CSR_ADJ_NARROW")) return g;
     g.wide = true;
     g.nyt = (ny + ADJW_MAX_N - 1) / ADJW_MAX_N;
-    g.N = ((ny + g.nyt - 1) / g.nyt + 15) / 16 * 16;
+    // a multiple of 32: each of the two epilogue warps of a lane quarter
+    // drains (N - 128) / 2 columns >= 128 in 16-column loads
+    g.N = ((ny + g.nyt - 1) / g.nyt + 31) / 32 * 32;
     // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128)
     g.NA = std::min(4, (512 - g.N - (g.N - 128)) / 64);
     // B ring: two stages (the MMAs take ~1.3 us per K block, an L2-hit TMA
@@ -244,6 +246,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
     tc.kb_total = (int)(tc.Mk / 32);
     const AdjGeom ag = tc_adj_geom(ny, Cp, tc.mt_a);
+    tc.nyA = std::max(tc.nyA, ag.nyt * ag.N);  // the wide tiles' padded pixel rows
     tc.adj_w = ag.wide;
     tc.adjw_CL = ag.CL;
     tc.adjw_N = ag.N;
@@ -278,8 +281,10 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         tc.adjw_smem = fixed + tc.adjw_nraw * tc.adj_stage;
         // the combine's sums [N][ADJ_SUM_LD] floats over the B and input rings
         const int rings = fixed - 1536 + tc.adjw_nraw * tc.adj_stage;
-        if (tc.adjw_nraw < 2 || tc.adjw_N * ADJ_SUM_LD * 4 > rings)
-            tc.adj_w = false;  // keep the narrow kernel
+        if (tc.adjw_nraw < 2 || tc.adjw_N * ADJ_SUM_LD * 4 > rings) {
+            tc.adj_w = false;  // keep the narrow kernel (128-row tiles)
+            tc.nyA = (ny + 127) / 128 * 128;
+        }
     }
     if (tc.adj_smem > 227 * 1024 || tc.fwd_smem > 227 * 1024) return 0;
 
@@ -529,6 +534,7 @@ inline int tc_adjoint(TcPlan &tc, const float2 *user, float2 *ws, cudaStream_t s
         P.NA = tc.adjw_NA;
         P.NB = tc.adjw_NB;
         P.exp_flags = tc.aexp;
+        P.trace = tc.trace;
         P.probe = tc.probe ? tc.probe + 4 * PROBE_ADJ : nullptr;
         P.kb_total = tc.kb_total;
         P.raw_bytes = tc.raw_bytes;

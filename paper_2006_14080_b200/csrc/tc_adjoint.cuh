@@ -98,7 +98,10 @@ __device__ __forceinline__ void wait_fast(uint64_t *b, uint32_t ph) {
 }
 constexpr int ADJ_SPW = 32 * 4 / ADJ_GW;
 constexpr int ADJ_W_EPI = 4 + ADJ_GW;
-constexpr int ADJ_THREADS = (ADJ_W_EPI + 4) * 32;
+// epilogue warps: two per TMEM lane quarter, each draining half of the 128
+// pixel rows of every chain (the drain stalls the MMAs: one accumulator pair)
+constexpr int ADJ_EW = 8;
+constexpr int ADJ_THREADS = (ADJ_W_EPI + ADJ_EW) * 32;
 constexpr int ADJ_SUM_LD = 129;                       // padded row (floats)
 constexpr int ADJ_SUM_BYTES = 128 * ADJ_SUM_LD * 4;   // fp32 sums [y][lane]
 static_assert(ADJ_SUM_BYTES <= ADJ_STAGES * ADJ_B_STAGE, "sums reuse the B ring");
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             mbar_init(&rempty[r], ADJ_GW);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 4);
+        mbar_init(acc_empty, ADJ_EW);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -381,23 +384,24 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
             ADJ_TL(3, lane == 0 && warp == 4);
         }
     }
-    float sum[128];  // epilogue warps: running sums of row m over the 128 y
+    float sum[64];  // epilogue warps: running sums of row m over their 64 y
+    const int eh = (warp - ADJ_W_EPI) >> 2;  // which half of the y rows
     if (run && warp >= ADJ_W_EPI) {
         // ---- epilogue: drain every chain into the register sums
         const int q = warp & 3;
-        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + 64 * eh;
 #pragma unroll
-        for (int y = 0; y < 128; ++y) sum[y] = 0.f;
+        for (int y = 0; y < 64; ++y) sum[y] = 0.f;
         for (int ch = 0; ch < nchain; ++ch) {
             wait_slow(acc_full, ch & 1);
             tc_fence_after();
 #pragma unroll
-            for (int cb = 0; cb < 8; ++cb) {
+            for (int cb = 0; cb < 4; ++cb) {
                 uint32_t rh[16], rl[16];
                 tmem_ld16(lane_base + cb * 16, rh);
                 tmem_ld16(lane_base + 128 + cb * 16, rl);
                 tmem_ld_wait();
-                if (cb == 7) {  // accumulator fully read: let the MMA go on
+                if (cb == 3) {  // this warp's accumulator columns read: let the MMA go on
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty);
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(ADJ_THREADS, 1)
     if (run && warp >= ADJ_W_EPI) {
         const int m = (warp & 3) * 32 + lane;
 #pragma unroll
-        for (int y = 0; y < 128; ++y) sum_s[y * ADJ_SUM_LD + m] = sum[y];
+        for (int y = 0; y < 64; ++y) sum_s[(64 * eh + y) * ADJ_SUM_LD + m] = sum[y];
     }
     __syncthreads();
     // ---- combine: ws[x, y] = sum_c conj(s_c[x,y]) (re + i im)_{x,c}(y), all

@@ -14,14 +14,14 @@
 //   TMEM: [0, N) D | [N, N + 64 NA) A stages (hi 32 | lo 32) | [.., + N-128) S
 // Chains of P.chain K blocks (shorter than k_tc_adjoint's: three MMAs per
 // K step now truncate into the same fp32 accumulator) are drained by the
-// four epilogue warps: columns [0, 128) into fp32 register sums, columns
+// eight epilogue warps: columns [0, 128) into fp32 register sums, columns
 // [128, N) into the TMEM sum region S (tcgen05.ld D, ld S, add, st S).
 // The end of the k range goes through shared memory (over the idle B ring)
 // into the coil combine, as k_tc_adjoint.
 //
-// Roles (12 warps): 0 lane 0 B-ring TMA, lane 1 input-ring TMA; 1 MMA
+// Roles (16 warps): 0 lane 0 B-ring TMA, lane 1 input-ring TMA; 1 MMA
 // issuer (elected lane); 2-3 input prep (d'); 4-7 generators (one per TMEM
-// lane quarter, 32 samples each); 8-11 epilogue.
+// lane quarter, 32 samples each); 8-15 epilogue (two per lane quarter).
 //
 // CL = 2: CTA pairs along x (a cluster of two x tiles of the same frame,
 // y tile and k range) share the static B tiles: each CTA fetches half of
@@ -36,21 +36,35 @@
 namespace csr {
 
 constexpr int ADJW_MAX_N = 256;
-constexpr int ADJW_THREADS = 12 * 32;
+constexpr int ADJW_EW = 8;  // epilogue warps: two per TMEM lane quarter
+constexpr int ADJW_THREADS = (8 + ADJW_EW) * 32;
 
 struct AdjWParams {
     unsigned long long *probe;
     TcArgs a;
     int S, kb_per_split, kb_total, raw_bytes, n_raw, chain;
-    int N;        // pixel rows per CTA (multiple of 16, 128 < N <= 256)
+    int N;        // pixel rows per CTA (multiple of 32, 128 < N <= 256)
     int NA;       // A stages in TMEM
     int NB;       // B ring stages in shared memory
     int exp_flags;
+    unsigned long long *trace;  // CSR_TRACE + -DADJ_TIMELINE: CTA 0 per-block clock64 stamps
     const float2 *sens;
     float2 *ws;
     const float *scales;
     const int *gate;
 };
+
+// CTA-0 per-K-block timeline (tools/trace_adjw.py; -DADJ_TIMELINE=1 builds)
+#if ADJ_TIMELINE
+#define ADJW_TL(i, slot, cond)                                                         \
+    if (P.trace && (cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && \
+        (i) < 1024)                                                                    \
+    P.trace[65536 + 8 * (i) + (slot)] = clock64()
+#else
+#define ADJW_TL(i, slot, cond) \
+    do {                       \
+    } while (0)
+#endif
 
 // shared memory: B ring NB x (hi N x 128 B | lo N x 128 B), input ring,
 // barriers; the coil-combine sums [N][ADJ_SUM_LD] floats reuse the B ring
@@ -114,7 +128,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             mbar_init(&rempty[r], GW);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 4);
+        mbar_init(acc_empty, ADJW_EW);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -204,7 +218,9 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             for (int i0 = i; i < iend; ++i) {
                 const int sa = i % NA, sb = i % NB;
                 wait_fast(&gen[sa], (i / NA) & 1);
+                ADJW_TL(i, 0, lane == 0);
                 wait_fast(&bfull[sb], (i / NB) & 1);
+                ADJW_TL(i, 1, lane == 0);
                 tc_fence_after();
                 const uint32_t st = smem_u32(smem + sb * BST);
                 const uint32_t a_hi = tmem + a_col0 + 64 * sa, a_lo = a_hi + 32;
@@ -239,6 +255,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         for (int i = 0, r = 0, rph = 0; i < nkb; ++i) {
             const int sa = i % NA;
             wait_fast(&dfull[r], rph);
+            ADJW_TL(i, 2, lane == 0 && warp == 4);
             const uint8_t *in = in_base + r * IN_STAGE;
             const float2 *p0s = reinterpret_cast<const float2 *>(in);
             const float2 *dps = reinterpret_cast<const float2 *>(in + OFF_DP) + (c * 2 + part);
@@ -264,7 +281,9 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                 r = 0;
                 rph ^= 1;
             }
+            ADJW_TL(i, 3, lane == 0 && warp == 4);
             wait_fast(&aempty[sa], ((i / NA) & 1) ^ 1);
+            ADJW_TL(i, 4, lane == 0 && warp == 4);
             tc_fence_after();
             const uint32_t col = lane_base + a_col0 + 64 * sa;
             tmem_st32(col, hv);
@@ -273,60 +292,73 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[sa]);
+            ADJW_TL(i, 5, lane == 0 && warp == 4);
         }
     }
-    float sum[128];  // epilogue warps: running sums of row m over y in [0, 128)
+    // Epilogue: two warps per TMEM lane quarter (h = 0, 1), each draining
+    // half of the columns of every chain: y in [64h, 64h + 64) into fp32
+    // register sums, and half of the columns >= 128 into the TMEM sums S.
+    // (The drain stalls the MMAs — one accumulator — so its length is the
+    // chain overhead: measured 2734 cycles per chain at config 4 with four
+    // warps reading 256 columns each, one TMEM round trip per 8-16 columns.)
+    float sum[64];
+    const int ew = warp - (4 + GW), eh = ew >> 2;
+    const int U2 = (N - 128) / 2;  // columns >= 128 per epilogue warp
     if (run && warp >= 4 + GW) {
         const int q = warp & 3;
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t dlo = lane_base + 64 * eh;                 // this warp's y < 128
+        const uint32_t dhi = lane_base + 128 + U2 * eh;           // its y >= 128
+        const uint32_t shi = lane_base + s_col0 + U2 * eh;        // their running sums
 #pragma unroll
-        for (int y = 0; y < 128; ++y) sum[y] = 0.f;
-        const int nhi = (N - 128) / 8;  // 8-column chunks of y >= 128
+        for (int y = 0; y < 64; ++y) sum[y] = 0.f;
         for (int ch = 0; ch < nchain; ++ch) {
             wait_slow(acc_full, ch & 1);
+            ADJW_TL(ch * chain, 6, lane == 0 && warp == 4 + GW);
             tc_fence_after();
 #pragma unroll
-            for (int cb = 0; cb < 8; ++cb) {
-                uint32_t r[16];
-                tmem_ld16(lane_base + cb * 16, r);
+            for (int cb = 0; cb < 2; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(dlo + cb * 32, r);
                 tmem_ld_wait();
 #pragma unroll
-                for (int yy = 0; yy < 16; ++yy) sum[cb * 16 + yy] += __uint_as_float(r[yy]);
+                for (int yy = 0; yy < 32; ++yy) sum[cb * 32 + yy] += __uint_as_float(r[yy]);
             }
-            for (int cb = 0; cb < nhi; ++cb) {
-                uint32_t r[8], sv[8];
-                tmem_ld8(lane_base + 128 + cb * 8, r);
-                if (ch > 0) tmem_ld8(lane_base + s_col0 + cb * 8, sv);
+            for (int cb = 0; cb < U2; cb += 16) {
+                uint32_t r[16], sv[16];
+                tmem_ld16(dhi + cb, r);
+                if (ch > 0) tmem_ld16(shi + cb, sv);
                 tmem_ld_wait();
-                if (cb == nhi - 1) {  // accumulator fully read: let the MMA go on
+                if (cb + 16 >= U2) {  // this warp has read its accumulator columns
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(acc_empty);
+                    ADJW_TL(ch * chain, 7, lane == 0 && warp == 4 + GW);
                 }
 #pragma unroll
-                for (int yy = 0; yy < 8; ++yy)
+                for (int yy = 0; yy < 16; ++yy)
                     sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
                                              __uint_as_float(r[yy]));
-                tmem_st8(lane_base + s_col0 + cb * 8, sv);
+                tmem_st16(shi + cb, sv);
             }
             tmem_st_wait();
         }
     }
-    __syncthreads();  // all MMAs and TMA loads are done: the B ring is free
+    __syncthreads();  // all MMAs and TMA loads are done: the rings are free
     if (run && warp >= 4 + GW) {
         const int q = warp & 3;
         const int m = q * 32 + lane;
-        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t shi = tmem + ((uint32_t)(q * 32) << 16) + s_col0 + U2 * eh;
 #pragma unroll
-        for (int y = 0; y < 128; ++y) sum_s[y * ADJ_SUM_LD + m] = sum[y];
+        for (int y = 0; y < 64; ++y) sum_s[(64 * eh + y) * ADJ_SUM_LD + m] = sum[y];
         tc_fence_after();
-        for (int cb = 0; cb < (N - 128) / 8; ++cb) {
-            uint32_t sv[8];
-            tmem_ld8(lane_base + s_col0 + cb * 8, sv);
+        for (int cb = 0; cb < U2; cb += 16) {
+            uint32_t sv[16];
+            tmem_ld16(shi + cb, sv);
             tmem_ld_wait();
 #pragma unroll
-            for (int yy = 0; yy < 8; ++yy)
-                sum_s[(128 + cb * 8 + yy) * ADJ_SUM_LD + m] = __uint_as_float(sv[yy]);
+            for (int yy = 0; yy < 16; ++yy)
+                sum_s[(128 + U2 * eh + cb + yy) * ADJ_SUM_LD + m] = __uint_as_float(sv[yy]);
         }
     }
     __syncthreads();
