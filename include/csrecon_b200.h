@@ -163,6 +163,15 @@ int csr_nudft_adjoint_sep(const void *phase0, const void *phase1_conj, const voi
  * (CSR_PLAN_ORDERED_SAMPLES; n_chunks = csr_plan_info.split_k).  Other
  * plans return their split-K partials. */
 int csr_adjoint_chunks(csr_plan *plan, const void *kdata, void *chunks, void *stream);
+/* The same with the k-space operand scale taken from a caller-supplied bound
+ * on the data (component-wise max |Re|, |Im| over ALL workers' chunks): the
+ * fp16 split's scale is an exact power of two of that bound, so chunk
+ * partials computed by different workers are bit-identical however the
+ * chunk maxima differ (csr_adjoint_chunks scales by this plan's own data;
+ * the native multi-rank loop max-allreduces the bound itself).  A bound
+ * below the plan's own max is raised to it. */
+int csr_adjoint_chunks_bound(csr_plan *plan, const void *kdata, void *chunks, float bound,
+                             void *stream);
 
 /* normal_operator (solver.py:128-139) without the allreduce:
  * out = F^H F x + (beta/2) Theta^H Theta x. */

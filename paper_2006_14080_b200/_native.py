@@ -84,6 +84,7 @@ SIGNATURES = {
     "csr_forward": [_P, _P, _P, _P],
     "csr_adjoint": [_P, _P, _P, _P],
     "csr_adjoint_chunks": [_P, _P, _P, _P],
+    "csr_adjoint_chunks_bound": [_P, _P, _P, _F, _P],
     "csr_sample_chunking": [_I32, _I32, _I32, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I32)],
     "csr_normal": [_P, _P, _P, _D, _P],
     "csr_theta": [_I32, _I32, _I32, _P, _P, _P],

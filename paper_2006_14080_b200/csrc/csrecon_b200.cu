@@ -513,6 +513,12 @@ int enqueue_admm_iteration(csr_plan *p, const AdmmBufs &b, int cg_max,
     return CSR_OK;
 }
 
+// scales[5] <- max(bound, scales[5]) (csr_adjoint_chunks_bound)
+__global__ void k_set_bound(float *s5, float bound) {
+    pdl_enter();
+    if (threadIdx.x == 0) *s5 = fmaxf(*s5, bound);
+}
+
 __global__ void k_flush(uint4 *buf, int64_t n, unsigned v) {
     pdl_enter();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1308,6 +1314,25 @@ int csr_adjoint_chunks(csr_plan *p, const void *kdata, void *chunks, void *strea
         return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
     g_launches.fetch_add(p->tc.adj_launches + 1, std::memory_order_relaxed);
     return mark_use(p, (cudaStream_t)stream);
+}
+
+int csr_adjoint_chunks_bound(csr_plan *p, const void *kdata, void *chunks, float bound,
+                             void *stream) {
+    if (!p || !kdata || !chunks) return fail(CSR_ERR_ARG, "null argument");
+    if (!p->tc.enabled) return fail(CSR_ERR_ARG, "chunk partials need the tensor-core operator");
+    if (!(bound > 0.f) || !std::isfinite(bound)) return fail(CSR_ERR_ARG, "bound must be > 0");
+    CU(cudaSetDevice(p->dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    tc_load_kd(p->tc, (const float2 *)kdata, st);
+    LAUNCHED();
+    // the operand scale from the caller's bound (every worker passes the same
+    // one), never below this worker's own max|kd| (fp16 range)
+    launch(k_set_bound, 1, 32, 0, st, p->tc.scales + 5, bound);
+    LAUNCHED();
+    if (tc_adjoint(p->tc, nullptr, (float2 *)chunks, st, nullptr))
+        return fail(CSR_ERR_CUDA, "tc adjoint launch: " + tc_last_error());
+    g_launches.fetch_add(p->tc.adj_launches, std::memory_order_relaxed);
+    return mark_use(p, st);
 }
 
 // One-shot separable NUDFT with the reference's kernel signatures

@@ -174,15 +174,25 @@ class DftOperator:
                      _dev.stream_ptr(self.device))
         return _dev.out_like(out, data)
 
-    def adjoint_chunks(self, data):
+    def adjoint_chunks(self, data, data_bound=None):
         """Per-chunk adjoint partials (n_chunks, nx, ny), unsummed
-        (ChunkedDftOperator.adjoint, operators.py:254-265)."""
+        (ChunkedDftOperator.adjoint, operators.py:254-265).
+
+        data_bound: a bound on max(|Re|, |Im|) of the data of ALL workers
+        (e.g. an allreduce-max of the workers' maxima).  With it, every
+        worker's fp16 operand scale is the same power of two and each chunk
+        partial is bit-identical whichever worker computes it; without it,
+        the scale follows this worker's own data."""
         if self.n_frames != 1:
             raise ValueError("chunk partials are defined for static (single-frame) plans")
         y = _dev.as_c64(data, (self.n_samples, self.n_coils), "data", self.device)
         out = _dev.empty_c64((self.info()["split_k"], self.nx, self.ny), self.device)
-        _native.call("csr_adjoint_chunks", self._plan, y.data_ptr(), out.data_ptr(),
-                     _dev.stream_ptr(self.device))
+        if data_bound is None:
+            _native.call("csr_adjoint_chunks", self._plan, y.data_ptr(), out.data_ptr(),
+                         _dev.stream_ptr(self.device))
+        else:
+            _native.call("csr_adjoint_chunks_bound", self._plan, y.data_ptr(), out.data_ptr(),
+                         float(data_bound), _dev.stream_ptr(self.device))
         return _dev.out_like(out, data)
 
     def normal(self, x, beta=0.0):
@@ -267,8 +277,10 @@ class ChunkedDftOperator:
     def forward(self, image):
         return self.op.forward(image)
 
-    def adjoint(self, data):
-        return self.op.adjoint_chunks(data)
+    def adjoint(self, data, data_bound=None):
+        """Chunk partials; pass the same data_bound on every worker for
+        partials that are bitwise independent of the worker split."""
+        return self.op.adjoint_chunks(data, data_bound)
 
 
 def build_factors(trajectory, grid, precision="single", device=None):

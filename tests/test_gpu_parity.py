@@ -399,6 +399,33 @@ def test_ordered_chunks_bitwise_for_every_split(cuda, nx, ny, nc, m):
     assert rel_err(ref, O.adjoint_sep(p0, p1, sens.astype(complex), data.astype(complex))) <= OP_TOL
 
 
+def test_ordered_chunks_bitwise_with_a_shared_bound(cuda):
+    # chunk maxima in different binades: each worker's own max|data| would
+    # give it a different fp16 operand scale; with the same data_bound on
+    # every worker the partials are bitwise independent of the split
+    nx, ny, nc, m = 96, 80, 3, 10000
+    grid = P.ImageGrid(nx, ny)
+    coords, sens, img, data = _ordered_problem(nx, ny, nc, m, 7)
+    chunk, n_chunks = P.sample_chunking(grid, nc, m)
+    assert n_chunks >= 3
+    for i in range(n_chunks):  # chunk i scaled by 8^i: a different binade each
+        data[i * chunk:(i + 1) * chunk] *= np.float32(8.0 ** i)
+    bound = float(np.max(np.abs(np.stack([data.real, data.imag]))))
+    ranges = [(i * chunk, min((i + 1) * chunk, m)) for i in range(n_chunks)]
+    full = P.ChunkedDftOperator.build(coords, grid, sens, ranges, range(n_chunks))
+    c_all = full.adjoint(data, data_bound=bound)
+    for world in (2, 3):
+        plan = P.make_shard_plan(m, world, chunk_size=chunk)
+        for r in range(world):
+            ids, rr = plan.worker_chunks(r)
+            op = P.ChunkedDftOperator.build(coords, grid, sens, rr, ids)
+            s0, s1 = plan.bounds[r]
+            assert np.array_equal(op.adjoint(data[s0:s1], data_bound=bound), c_all[list(ids)])
+    p0, p1 = O.build_factors(coords, nx, ny, "double")
+    ref = O.adjoint_sep(p0, p1, sens.astype(complex), data.astype(complex))
+    assert rel_err(c_all.astype(np.complex128).sum(0), ref) <= OP_TOL
+
+
 def test_sample_shard_admm_matches_reference(cuda):
     # shard="sample" on one rank: the order-stable plan (tile-group forward,
     # chunked adjoint, fold in chunk order) through the native ADMM loop

@@ -132,3 +132,41 @@ def test_harness_configs_match_baseline_shapes():
     assert abs(nudft_flops_per_cg(0) / 1e9 - 1.074) < 1e-3
     assert abs(nudft_flops_per_cg(2) / 1e9 - 1099.5) < 0.1
     assert abs(nudft_flops_per_cg(4) / 1e9 - 11545) < 1
+
+
+def test_order_stable_shard_resolution():
+    # solver.py:281-297: order_stable=True (the reference's default) makes
+    # the image bitwise independent of n_workers; on several ranks a static
+    # problem's shard="auto" therefore becomes the order-stable sample split
+    from paper_2006_14080_b200.solver import resolve_shard
+    assert resolve_shard("auto", True, 1, 4) == "sample"
+    assert resolve_shard("auto", False, 1, 4) == "auto"
+    assert resolve_shard("auto", True, 1, 1) == "auto"
+    assert resolve_shard("auto", True, 8, 4) == "auto"      # 2-D+t: frames
+    with pytest.warns(UserWarning, match="not bitwise independent"):
+        assert resolve_shard("coil", True, 1, 2) == "coil"
+
+
+def test_collective_argument_is_validated():
+    from paper_2006_14080_b200.solver import _Shard
+    with pytest.raises(ValueError, match="collective"):
+        _Shard(None, np.zeros((1, 2, 2)), 1, "auto", None, collective="mpi")
+
+
+def test_refbind_installs_into_a_kernel_table():
+    # the reference's plug-in point (kernels.py:212-274): the "cuda" table
+    # replaces the active one and can be removed again; building the table
+    # touches no device
+    import types
+    import paper_2006_14080_b200.refbind as rb
+    numpy_table = {"forward_sep": None}
+    k = types.SimpleNamespace(_IMPL={"numpy": numpy_table}, _ACTIVE=numpy_table,
+                              _BACKEND="numpy")
+    prev = rb.install(k)
+    assert k._BACKEND == "cuda" and k._ACTIVE is k._IMPL["cuda"]
+    assert set(k._ACTIVE) >= {"forward_mat", "adjoint_mat", "forward_sep", "adjoint_sep",
+                              "theta", "theta_adj", "soft"}
+    with pytest.raises(NotImplementedError, match="separable"):
+        k._ACTIVE["forward_mat"](None, None, None)
+    rb.uninstall(k, prev)
+    assert k._BACKEND == "numpy" and k._ACTIVE is numpy_table and "cuda" not in k._IMPL
