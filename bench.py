@@ -221,12 +221,13 @@ def run_reference(args, cfg, world, rank):
     prob = make_problem(cfg, encoder=input_encoder(cfg))
     arm = CpuArm(prob)
     arm.seconds(1)  # numba JIT / BLAS warm-up
-    for _ in range(args.warmup):
-        arm.seconds(1)
-    times = [arm.seconds(1) for _ in range(args.steps)]
-    total = float(np.sum(times)) * arm.frames_scale
+    arm.seconds(max(1, args.warmup))
+    # the K timed steps are K consecutive ADMM iterations of one call (the
+    # reference's solve loop; its per-call setup is outside solve_seconds)
+    total = arm.seconds(args.steps) * arm.frames_scale
     value = args.steps / total
-    sample = (f"config {cfg}: {args.steps} steps of 1 ADMM iteration (CG = 5) each; "
+    sample = (f"config {cfg}: {args.steps} steps = {args.steps} consecutive ADMM iterations "
+              f"(CG = 5) of one call, after a {max(1, args.warmup)}-iteration warm-up call; "
               f"{arm.desc}")
     return {"metric": METRIC, "value": value, "unit": "iter/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
