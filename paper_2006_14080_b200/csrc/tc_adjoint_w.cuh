@@ -266,7 +266,11 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             } else
 #pragma unroll
             for (int k = 0; k < SPW; ++k) {
-                const float2 p = p0s[k * XS + xl], u = dps[k * CP * 2];
+                // (profiling, debug builds: 4 = operands from registers, no LDS)
+                const float2 p = (P.exp_flags & 4) ? make_float2(0.6f + 1e-3f * k, 0.8f)
+                                                   : p0s[k * XS + xl];
+                const float2 u = (P.exp_flags & 4) ? make_float2(1e-2f * lane, 0.5f * k)
+                                                   : dps[k * CP * 2];
                 const float e0 = fmaf(p.x, u.x, p.y * u.y);
                 const float e1 = fmaf(p.y, u.x, -(p.x * u.y));
                 const __half2 hh = __floats2half2_rn(e0, e1);
@@ -286,9 +290,11 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             ADJW_TL(i, 4, lane == 0 && warp == 4);
             tc_fence_after();
             const uint32_t col = lane_base + a_col0 + 64 * sa;
-            tmem_st32(col, hv);
-            tmem_st32(col + 32, lv);
-            tmem_st_wait();
+            if (!(P.exp_flags & 8)) {  // (profiling: 8 = no TMEM stores)
+                tmem_st32(col, hv);
+                tmem_st32(col + 32, lv);
+                tmem_st_wait();
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&gen[sa]);

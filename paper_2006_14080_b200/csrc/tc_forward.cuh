@@ -28,7 +28,7 @@ struct FwdParams {
     float2 *kdp;  // [G][T][Mk][Cp]
     const float *scales;
     const int *gate;
-    int exp_flags;  // profiling (debug builds, CSR_FEXP): 1 no MMA, 2 no TMA
+    int exp_flags;  // profiling (debug builds, CSR_FEXP): 1 no MMA, 2 no TMA, 4 no drain
 };
 
 
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + ab * TC_BN;
             const int xbase = nt * P.a.xs;
-            for (int chb = 0; chb < 8; chb += U) {
+            for (int chb = (P.exp_flags & 4) ? 8 : 0; chb < 8; chb += U) {
                 float2 p0v[16 * U / CP > 0 ? 16 * U / CP : 1];
 #pragma unroll
                 for (int i = 0; i < 16 * U / CP; ++i) {
