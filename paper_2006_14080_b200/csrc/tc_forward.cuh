@@ -14,10 +14,6 @@ namespace csr {
 #define FWD_ELECT 1
 #endif
 __device__ __forceinline__ bool fwd_one() { return FWD_ELECT ? sm100::elect_one() : true; }
-#ifndef FWD_SS_ELECT
-#define FWD_SS_ELECT 0
-#endif
-__device__ __forceinline__ bool fwd_ss_one() { return FWD_SS_ELECT ? sm100::elect_one() : true; }
 
 struct FwdParams {
     unsigned long long *probe;  // live timing slot (probe_enter/exit) or null
@@ -32,12 +28,20 @@ struct FwdParams {
 };
 
 
-// CL = 2: pairs of consecutive sample tiles of the same frame (a cluster
-// along x) share the image operand B: each CTA fetches half of the 256 B
-// rows of every K block and multicasts them to both CTAs, so the L2 -> SM
-// traffic per K block drops from 96 to 64 KiB per CTA.  A stage is
-// refilled only after the MMAs of both CTAs released it (multicast commit
-// onto the pair's `empty` barriers, which count CL arrivals).
+// CL = 2: a CTA pair (cta_group::2) on two consecutive sample tiles of the
+// same frame: M = 256 pair MMAs, each CTA's shared memory holds its 128
+// sample rows of A and HALF (128) of the 256 doubled image rows of B, so the
+// shared-memory traffic per SM per K block drops from 96 KiB of TMA writes
+// + 32 KiB of MMA reads per K16 to 64 + 20 KiB — the single-CTA form is
+// bound by that port (tools/mma_micro.cu: 14970 vs 12570 cycles per
+// 128 x 128 x 256 complex tile, MMA floor 12288).  The leader (rank 0)
+// issues the MMAs; both CTAs' TMA loads complete on the leader's `full`
+// barrier (cta_group::2 form); MMA commits are multicast onto both CTAs'
+// `empty` / `tfull` barriers; both CTAs' epilogues release an accumulator
+// on the leader's `tempty`.  Three 64 KiB stages per CTA.
+constexpr int FWD_PAIR_STAGE = 2 * TC_A_TILE + TC_B_TILE;  // A hi/lo + B hi/lo halves
+constexpr int FWD_PAIR_STAGES = 3;
+static_assert(FWD_PAIR_STAGES * FWD_PAIR_STAGE <= TC_STAGES * TC_FWD_OPS, "pair stages fit");
 template <int CP, int CL>
 __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     k_tc_forward(const __grid_constant__ CUtensorMap tmA_hi,
@@ -49,11 +53,15 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     // (the gate is uniform over the grid, so a pair leaves together)
     if (P.gate && !*P.gate) return;
     probe_enter(P.probe);
+    constexpr bool PAIR = CL > 1;
+    constexpr int STAGE = PAIR ? FWD_PAIR_STAGE : TC_FWD_OPS;
+    constexpr int NSTG = PAIR ? FWD_PAIR_STAGES : TC_STAGES;
+    constexpr int BH = PAIR ? TC_B_TILE / 2 : TC_B_TILE;  // B bytes (hi or lo) per CTA
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + TC_STAGES * TC_FWD_OPS);
-    uint64_t *empty = full + TC_STAGES;
-    uint64_t *tfull = empty + TC_STAGES;
+    uint64_t *empty = full + NSTG;
+    uint64_t *tfull = empty + NSTG;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
@@ -68,61 +76,69 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
         tma_prefetch(&tmA_lo);
         tma_prefetch(&tmB_hi);
         tma_prefetch(&tmB_lo);
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < NSTG; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CL);
+            mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 4 * CL);
         }
-        fence_barrier_init();
+        if (PAIR) fence_barrier_init_cluster();
+        else fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
-    if (CL > 1) cluster_sync();  // the peer's barriers exist before any multicast
+    if (PAIR) cluster_sync();  // the leader's barriers exist before any remote use
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0;
 
     if (warp == 0) {
         if (lane == 0) {
+            // the leader's stage barriers (shared::cluster addresses)
+            const uint32_t lead_full = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
             int it = 0;
             for (int nt = nt0; nt < nt1; ++nt) {
                 const int brow = t * P.a.Nf + nt * TC_BN;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % TC_STAGES;
-                    const uint32_t ph = (it / TC_STAGES) & 1;
+                    const int s = it % NSTG;
+                    const uint32_t ph = (it / NSTG) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t *st = smem + s * TC_FWD_OPS;
+                    uint8_t *st = smem + s * STAGE;
                     if (P.exp_flags & 2) {
-                        mbar_arrive(&full[s]);
+                        if (crank == 0) mbar_arrive(&full[s]);
                         continue;
                     }
-                    mbar_arrive_expect_tx(&full[s], TC_FWD_OPS);
-                    tma_load_2d(st, &tmA_hi, &full[s], kb * 64, mtile * TC_BM);
-                    tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, mtile * TC_BM);
-                    if (CL == 1) {
+                    if (!PAIR) {
+                        mbar_arrive_expect_tx(&full[s], TC_FWD_OPS);
+                        tma_load_2d(st, &tmA_hi, &full[s], kb * 64, mtile * TC_BM);
+                        tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[s], kb * 64, mtile * TC_BM);
                         tma_load_2d(st + 2 * TC_A_TILE, &tmB_hi, &full[s], kb * 64, brow);
                         tma_load_2d(st + 2 * TC_A_TILE + TC_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
                     } else {
-                        const int o = (int)crank * (TC_BN / CL);
-                        const uint16_t mask = (uint16_t)((1u << CL) - 1);
-                        tma_load_2d_mc(st + 2 * TC_A_TILE + o * 128, &tmB_hi, &full[s], kb * 64,
-                                       brow + o, mask);
-                        tma_load_2d_mc(st + 2 * TC_A_TILE + TC_B_TILE + o * 128, &tmB_lo, &full[s],
-                                       kb * 64, brow + o, mask);
+                        // the leader arms its barrier for both CTAs' bytes (the
+                        // peer's copies may complete first: tx-count goes
+                        // transiently negative within the phase)
+                        if (crank == 0) mbar_arrive_expect_tx(&full[s], CL * STAGE);
+                        const uint32_t fb = lead_full + s * 8;
+                        const int bro = brow + (int)crank * (TC_BN / 2);
+                        tma_load_2d_pair(st, &tmA_hi, fb, kb * 64, mtile * TC_BM);
+                        tma_load_2d_pair(st + TC_A_TILE, &tmA_lo, fb, kb * 64, mtile * TC_BM);
+                        tma_load_2d_pair(st + 2 * TC_A_TILE, &tmB_hi, fb, kb * 64, bro);
+                        tma_load_2d_pair(st + 2 * TC_A_TILE + BH, &tmB_lo, fb, kb * 64, bro);
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        // the whole warp runs the issue loop, one elected lane issues
-        // (warp-uniform descriptors: no per-MMA waterfall) when FWD_SS_ELECT;
-        // measured neutral-to-slower for this form (configs 2, 3), so off
-        if (FWD_SS_ELECT || lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(TC_BM, TC_BN);
+        // MMA issue: lane 0 of the (leader) CTA
+        if (lane == 0 && crank == 0) {
+            constexpr uint32_t idesc = idesc_f16(TC_BM * CL, TC_BN);
             int it = 0, tc = 0;
             for (int nt = nt0; nt < nt1; ++nt, ++tc) {
                 const int ab = tc & 1;
@@ -131,31 +147,34 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                 tc_fence_after();
                 const uint32_t dcol = tmem + ab * TC_BN;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % TC_STAGES;
-                    const uint32_t ph = (it / TC_STAGES) & 1;
+                    const int s = it % NSTG;
+                    const uint32_t ph = (it / NSTG) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * TC_FWD_OPS);
+                    const uint32_t st = smem_u32(smem + s * STAGE);
                     const uint32_t a_hi = st, a_lo = st + TC_A_TILE;
-                    const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + TC_B_TILE;
-                    if (fwd_ss_one()) {
+                    const uint32_t b_hi = st + 2 * TC_A_TILE, b_lo = b_hi + BH;
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            if (P.exp_flags & 1) break;
-                            const uint32_t o = kk * 32;
-                            const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
-                            const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if (P.exp_flags & 1) break;
+                        const uint32_t o = kk * 32;
+                        const uint64_t dah = desc_sw128(a_hi + o), dal = desc_sw128(a_lo + o);
+                        const uint64_t dbh = desc_sw128(b_hi + o), dbl = desc_sw128(b_lo + o);
+                        if (PAIR) {
+                            mma_f16_pair<1>(dcol, dah, dbh, idesc, (kb | kk) != 0);
+                            mma_f16_pair<2>(dcol, dah, dbl, idesc, 1);
+                            mma_f16_pair<0>(dcol, dal, dbh, idesc, 1);
+                        } else {
                             mma_f16_fill(dcol, dah, dbh, idesc, (kb | kk) != 0);
                             mma_f16_lastuse(dcol, dah, dbl, idesc, 1);
                             mma_f16(dcol, dal, dbh, idesc, 1);
                         }
-                        if (CL > 1) mma_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1));
-                        else mma_commit(&empty[s]);
                     }
-                    if (FWD_SS_ELECT) __syncwarp();
+                    if (PAIR) mma_commit_pair_mc(&empty[s], (uint16_t)((1u << CL) - 1));
+                    else mma_commit(&empty[s]);
                 }
-                if (fwd_ss_one()) mma_commit(&tfull[ab]);
-                if (FWD_SS_ELECT) __syncwarp();
+                if (PAIR) mma_commit_pair_mc(&tfull[ab], (uint16_t)((1u << CL) - 1));
+                else mma_commit(&tfull[ab]);
             }
         }
     } else {
@@ -200,7 +219,10 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[ab]);
+            if (lane == 0) {
+                if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[ab]), 0));
+                else mbar_arrive(&tempty[ab]);
+            }
         }
         if (P.amax) {  // max|kd| for the adjoint's operand scale (order-free)
             float mx = 0.f;
@@ -222,11 +244,13 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     }
     __syncthreads();
     probe_exit(P.probe);
-    // no CTA of a pair leaves while the peer's MMA commits may still arrive
-    if (CL > 1) cluster_sync();
+    // no CTA of a pair leaves while the leader's MMAs / commits may still
+    // touch the peer (its shared memory, barriers and tensor memory)
+    if (PAIR) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if (PAIR) tmem_dealloc_pair(tmem, 512);
+        else tmem_dealloc(tmem, 512);
     }
 }
 

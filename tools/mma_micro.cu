@@ -284,6 +284,329 @@ void run_pipe(unsigned long long *d_out, const uint8_t *g, size_t gbytes, const 
            TM == 0 ? "none" : TM == 1 ? "ld" : TM == 2 ? "st" : "ld+st", s / 148 / (nb * 12.0));
 }
 
+// Complex-GEMM tile forms, fed like the forward (bulk copies of operand
+// stages from an L2-resident source, full / empty barriers), with the
+// epilogue's TMEM drains.  One tile = 128 rows x 128 complex columns x 256
+// complex K (config 4's forward tile):
+//  DBL   the doubled-row form: 8 K blocks of [A_hi|A_lo] 16 KiB each +
+//        [B_hi|B_lo] 32 KiB each (96 KiB stages), 3 N = 256 MMAs per K16,
+//        two 256-column accumulators (drain of one overlaps the other);
+//  GAUSS three real products K1 = (Ar+Ai)Br, K2 = Ar(Bi-Br), K3 = Ai(Br+Bi):
+//        12 sub-stages of [A_hi|A_lo|B_hi|B_lo] 16 KiB each (64 KiB), 3 N = 128
+//        MMAs per K16 into accumulator j (columns 128 j), each accumulator
+//        released by the epilogue as soon as it is read (K1, K2, K3 order).
+// NEPI epilogue warps drain (tcgen05.ld) every accumulator of every tile.
+template <bool GAUSS, int NSTG, int NEPI>
+__global__ void k_cplx(int n_tiles, const uint8_t *gsrc, size_t gbytes, unsigned long long *out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    constexpr int STAGE = GAUSS ? 65536 : 98304;
+    constexpr int NSUB = GAUSS ? 12 : 8;   // stages per tile
+    constexpr int NACC = GAUSS ? 3 : 2;
+    constexpr int ACOL = GAUSS ? 128 : 256;
+    __shared__ uint64_t full[4], empty[4], tfull[3], tempty[3], done;
+    __shared__ uint32_t tslot;
+    __shared__ float sink;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTG; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int j = 0; j < 3; ++j) {
+            mbar_init(&tfull[j], 1);
+            mbar_init(&tempty[j], NEPI > 0 ? NEPI : 1);
+        }
+        mbar_init(&done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc(&tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (warp == 1 && lane == 0) {
+        int it = 0;
+        for (int t = 0; t < n_tiles; ++t)
+            for (int sb = 0; sb < NSUB; ++sb, ++it) {
+                const int s = it % NSTG;
+                mbar_wait(&empty[s], ((it / NSTG) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], STAGE);
+                const size_t off = ((size_t)(blockIdx.x * 977 + it) * STAGE) % (gbytes - STAGE);
+                bulk_g2s(sm + s * STAGE, gsrc + (off & ~(size_t)1023), STAGE, &full[s]);
+            }
+    } else if (warp == 0) {
+        const long long t0 = clock64();
+        int it = 0;
+        for (int t = 0; t < n_tiles; ++t) {
+            for (int sb = 0; sb < NSUB; ++sb, ++it) {
+                const int j = GAUSS ? sb % 3 : (t & 1);
+                const int use = GAUSS ? t : (t >> 1);   // uses of accumulator j so far
+                if ((GAUSS && sb < 3) || (!GAUSS && sb == 0)) {
+                    if (NEPI > 0) mbar_wait(&tempty[j], (use & 1) ^ 1);
+                    tc_fence_after();
+                }
+                const int s = it % NSTG;
+                mbar_wait(&full[s], (it / NSTG) & 1);
+                tc_fence_after();
+                const uint32_t st = smem_u32(sm + s * STAGE);
+                const uint32_t d = tmem + j * ACOL;
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t acc = GAUSS ? (sb >= 3 || kk > 0) : (sb > 0 || kk > 0);
+                        if (GAUSS) {
+                            constexpr uint32_t idesc = idesc_f16(128, 128);
+                            const uint64_t dah = desc_sw128(st + kk * 32), dal = desc_sw128(st + 16384 + kk * 32);
+                            const uint64_t dbh = desc_sw128(st + 32768 + kk * 32), dbl = desc_sw128(st + 49152 + kk * 32);
+                            mma_f16_fill(d, dah, dbh, idesc, acc);
+                            mma_f16_lastuse(d, dah, dbl, idesc, 1);
+                            mma_f16(d, dal, dbh, idesc, 1);
+                        } else {
+                            constexpr uint32_t idesc = idesc_f16(128, 256);
+                            const uint64_t dah = desc_sw128(st + kk * 32), dal = desc_sw128(st + 16384 + kk * 32);
+                            const uint64_t dbh = desc_sw128(st + 32768 + kk * 32), dbl = desc_sw128(st + 65536 + kk * 32);
+                            mma_f16_fill(d, dah, dbh, idesc, acc);
+                            mma_f16_lastuse(d, dah, dbl, idesc, 1);
+                            mma_f16(d, dal, dbh, idesc, 1);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                    if ((GAUSS && sb >= NSUB - 3) || (!GAUSS && sb == NSUB - 1)) mma_commit(&tfull[j]);
+                }
+                __syncwarp();
+            }
+        }
+        if (elect_one()) mma_commit(&done);
+        __syncwarp();
+        mbar_wait(&done, 0);
+        const long long t1 = clock64();
+        if (lane == 0) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+    } else if (warp >= 2 && warp < 2 + NEPI) {
+        const int e = warp - 2, q = warp & 3;
+        constexpr int SHARE = NEPI >= 4 ? ACOL / (NEPI / 4) : ACOL;  // columns per warp
+        const int c0 = NEPI >= 8 ? (e / 4) * SHARE : 0;
+        float acc = 0.f;
+        for (int t = 0; t < n_tiles; ++t) {
+            for (int jj = 0; jj < (GAUSS ? 3 : 1); ++jj) {
+                const int j = GAUSS ? jj : (t & 1);
+                const int use = GAUSS ? t : (t >> 1);
+                mbar_wait(&tfull[j], use & 1);
+                tc_fence_after();
+                const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + j * ACOL + c0;
+                for (int c = 0; c < SHARE; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(base + c, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[j]);
+            }
+        }
+        if (acc == 1.2345f) sink = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+template <bool GAUSS, int NSTG, int NEPI>
+void run_cplx(unsigned long long *d_out, const uint8_t *g, size_t gbytes) {
+    const int smem = NSTG * (GAUSS ? 65536 : 98304) + 1024;
+    cudaFuncSetAttribute(k_cplx<GAUSS, NSTG, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int nt = 64;
+    unsigned long long h[148];
+    for (int it = 0; it < 2; ++it) {
+        k_cplx<GAUSS, NSTG, NEPI><<<148, 64 + 32 * (NEPI > 0 ? NEPI : 0), smem>>>(nt, g, gbytes, d_out);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            printf("error %s\n", cudaGetErrorString(e));
+            return;
+        }
+    }
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int i = 0; i < 148; ++i) s += (double)h[i];
+    const double per_tile = s / 148 / nt;
+    printf("complex tile 128x128x256 %s, %d stages, %d drain warps: %7.0f cycles/tile (MMA floor %d)\n",
+           GAUSS ? "GAUSS (3 x N=128 products)" : "DBL (doubled rows, N=256)", NSTG, NEPI, per_tile,
+           GAUSS ? 9216 : 12288);
+}
+
+// The same tile forms on a CTA pair (cta_group::2): M = 256 (128 rows per
+// CTA), each CTA's stage holds its 128 A rows and HALF of the B rows, the
+// leader issues the pair MMAs.  Per SM: DBL 64 KiB stages (A hi/lo 16 KiB,
+// B hi/lo halves 16 KiB), GAUSS 48 KiB sub-stages (B halves 8 KiB).  The
+// peer's bulk copies complete on its own barrier and a relay lane forwards
+// the arrival to the leader (the real kernels use the cta_group::2 TMA form).
+__device__ __forceinline__ void mma_f16_pair_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                uint32_t acc, int coll) {
+    if (coll == 1)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+    else if (coll == 2)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+template <bool GAUSS, int NSTG, int NEPI>
+__global__ void __cluster_dims__(2, 1, 1) k_cplx2(int n_tiles, const uint8_t *gsrc, size_t gbytes,
+                                                  unsigned long long *out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    constexpr int BH = GAUSS ? 8192 : 16384;       // B half (hi or lo) per CTA
+    constexpr int STAGE = 32768 + 2 * BH;
+    constexpr int NSUB = GAUSS ? 12 : 8;
+    constexpr int ACOL = GAUSS ? 128 : 256;
+    __shared__ __align__(8) uint64_t full[4], full2[4], empty[4], tfull[3], tempty[3], done;
+    __shared__ uint32_t tslot;
+    __shared__ float sink;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTG; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&full2[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int j = 0; j < 3; ++j) {
+            mbar_init(&tfull[j], 1);
+            mbar_init(&tempty[j], NEPI > 0 ? 2 * NEPI : 1);
+        }
+        mbar_init(&done, 1);
+        fence_barrier_init_cluster();
+    }
+    if (warp == 0) tmem_alloc_pair(&tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (warp == 1 && lane == 0) {
+        int it = 0;
+        for (int t = 0; t < n_tiles; ++t)
+            for (int sb = 0; sb < NSUB; ++sb, ++it) {
+                const int s = it % NSTG;
+                mbar_wait(&empty[s], ((it / NSTG) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], STAGE);
+                const size_t off = ((size_t)(blockIdx.x * 977 + it) * STAGE) % (gbytes - STAGE);
+                bulk_g2s(sm + s * STAGE, gsrc + (off & ~(size_t)1023), STAGE, &full[s]);
+            }
+    } else if (warp == 0 && rank == 1 && lane == 0) {
+        // relay: the peer's stage landed -> the leader's full2
+        const uint32_t remote = mapa_shared(smem_u32(&full2[0]), 0);
+        int it = 0;
+        for (int t = 0; t < n_tiles; ++t)
+            for (int sb = 0; sb < NSUB; ++sb, ++it) {
+                const int s = it % NSTG;
+                mbar_wait(&full[s], (it / NSTG) & 1);
+                mbar_arrive_cluster(remote + s * 8);
+            }
+    } else if (warp == 0 && rank == 0) {
+        const long long t0 = clock64();
+        int it = 0;
+        for (int t = 0; t < n_tiles; ++t) {
+            for (int sb = 0; sb < NSUB; ++sb, ++it) {
+                const int j = GAUSS ? sb % 3 : (t & 1);
+                const int use = GAUSS ? t : (t >> 1);
+                if ((GAUSS && sb < 3) || (!GAUSS && sb == 0)) {
+                    if (NEPI > 0) mbar_wait(&tempty[j], (use & 1) ^ 1);
+                    tc_fence_after();
+                }
+                const int s = it % NSTG;
+                mbar_wait(&full[s], (it / NSTG) & 1);
+                mbar_wait(&full2[s], (it / NSTG) & 1);
+                tc_fence_after();
+                const uint32_t st = smem_u32(sm + s * STAGE);
+                const uint32_t d = tmem + j * ACOL;
+                if (elect_one()) {
+                    constexpr uint32_t idesc = idesc_f16(256, GAUSS ? 128 : 256);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t acc = GAUSS ? (sb >= 3 || kk > 0) : (sb > 0 || kk > 0);
+                        const uint64_t dah = desc_sw128(st + kk * 32), dal = desc_sw128(st + 16384 + kk * 32);
+                        const uint64_t dbh = desc_sw128(st + 32768 + kk * 32), dbl = desc_sw128(st + 32768 + BH + kk * 32);
+                        mma_f16_pair_ss(d, dah, dbh, idesc, acc, 1);
+                        mma_f16_pair_ss(d, dah, dbl, idesc, 1, 2);
+                        mma_f16_pair_ss(d, dal, dbh, idesc, 1, 0);
+                    }
+                    mma_commit_pair_mc(&empty[s], 3);
+                    if ((GAUSS && sb >= NSUB - 3) || (!GAUSS && sb == NSUB - 1)) mma_commit_pair_mc(&tfull[j], 3);
+                }
+                __syncwarp();
+            }
+        }
+        if (elect_one()) mma_commit_pair_mc(&done, 3);
+        __syncwarp();
+        mbar_wait(&done, 0);
+        const long long t1 = clock64();
+        if (lane == 0) out[blockIdx.x / 2] = (unsigned long long)(t1 - t0);
+    } else if (warp >= 2 && warp < 2 + NEPI) {
+        const int e = warp - 2, q = warp & 3;
+        constexpr int SHARE = NEPI >= 4 ? ACOL / (NEPI / 4) : ACOL;
+        const int c0 = NEPI >= 8 ? (e / 4) * SHARE : 0;
+        const uint32_t remote = mapa_shared(smem_u32(&tempty[0]), 0);
+        float acc = 0.f;
+        for (int t = 0; t < n_tiles; ++t) {
+            for (int jj = 0; jj < (GAUSS ? 3 : 1); ++jj) {
+                const int j = GAUSS ? jj : (t & 1);
+                const int use = GAUSS ? t : (t >> 1);
+                mbar_wait(&tfull[j], use & 1);
+                tc_fence_after();
+                const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + j * ACOL + c0;
+                for (int c = 0; c < SHARE; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld32(base + c, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(remote + j * 8);
+            }
+        }
+        if (acc == 1.2345f) sink = acc;
+    }
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem, 512);
+    }
+}
+
+template <bool GAUSS, int NSTG, int NEPI>
+void run_cplx2(unsigned long long *d_out, const uint8_t *g, size_t gbytes) {
+    const int smem = NSTG * (32768 + 2 * (GAUSS ? 8192 : 16384)) + 1024;
+    cudaFuncSetAttribute(k_cplx2<GAUSS, NSTG, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int nt = 64;
+    unsigned long long h[74];
+    for (int it = 0; it < 2; ++it) {
+        k_cplx2<GAUSS, NSTG, NEPI><<<148, 64 + 32 * NEPI, smem>>>(nt, g, gbytes, d_out);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            printf("error %s\n", cudaGetErrorString(e));
+            return;
+        }
+    }
+    cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int i = 0; i < 74; ++i) s += (double)h[i];
+    const double per_tile = s / 74 / nt;  // one pair tile = 2 single tiles of work
+    printf("PAIR complex tile 256x128x256 %s, %d stages, %d drain warps/CTA: %7.0f cycles/pair tile "
+           "(MMA floor %d)\n", GAUSS ? "GAUSS (3 x N=128 products)" : "DBL (doubled rows, N=256)", NSTG,
+           NEPI, per_tile, GAUSS ? 9216 : 12288);
+}
+
 template <int N, int NACC, bool TS>
 void run(unsigned long long *d_out) {
     const int smem = 16384 + 32768 + 1024;
@@ -306,9 +629,11 @@ void run(unsigned long long *d_out) {
            N, TS ? "TS" : "SS", NACC, cyc, 128 * N / 256, 128.0 * N * 16 / cyc);
 }
 
-int main() {
+int main(int argc, char **argv) {
+    const bool only_cplx = argc > 1;
     unsigned long long *d_out;
     cudaMalloc(&d_out, 148 * 8);
+    if (!only_cplx) {
     run<256, 1, false>(d_out);
     run<256, 2, false>(d_out);
     run<256, 1, true>(d_out);
@@ -325,11 +650,13 @@ int main() {
     run_pattern<true, 0>(d_out);
     run_pattern<false, 4>(d_out);
     run_pattern<true, 4>(d_out);
+    }
     uint8_t *g_small, *g_big;
     cudaMalloc(&g_small, 8 << 20);   // L2-resident source
     cudaMalloc(&g_big, 1ull << 31);  // 2 GiB: mostly HBM
     cudaMemset(g_small, 0x3c, 8 << 20);
     cudaMemset(g_big, 0x3c, 1ull << 31);
+    if (!only_cplx) {
     run_pipe<false, 2>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
     run_pipe<false, 3>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
     run_pipe<true, 2>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
@@ -338,5 +665,17 @@ int main() {
     run_pipe<false, 3, 1>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
     run_pipe<true, 3, 2>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
     run_pipe<true, 3, 3>(d_out, g_small, 8 << 20, "L2 (8 MiB)");
+    }
+    run_cplx<false, 2, 0>(d_out, g_small, 8 << 20);
+    run_cplx<false, 2, 4>(d_out, g_small, 8 << 20);
+    run_cplx<true, 3, 0>(d_out, g_small, 8 << 20);
+    run_cplx<true, 3, 4>(d_out, g_small, 8 << 20);
+    run_cplx<true, 3, 8>(d_out, g_small, 8 << 20);
+    run_cplx2<false, 3, 0>(d_out, g_small, 8 << 20);
+    run_cplx2<false, 3, 4>(d_out, g_small, 8 << 20);
+    run_cplx2<true, 4, 0>(d_out, g_small, 8 << 20);
+    run_cplx2<true, 4, 4>(d_out, g_small, 8 << 20);
+    run_cplx2<true, 4, 8>(d_out, g_small, 8 << 20);
+    run_cplx2<true, 3, 8>(d_out, g_small, 8 << 20);
     return 0;
 }
