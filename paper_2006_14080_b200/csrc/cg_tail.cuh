@@ -509,13 +509,20 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_cg_tail1(CgTailArgs A) {
         }
     };
     if ((!XOP || TAIL_PAIRS_XOP) && (g.ny & 1) == 0) {
-        // pixel pairs with 16-byte loads / stores (update() per pixel)
+        // pixel pairs with 16-byte loads / stores (update() per pixel).
+        // The pass runs from the END of the vectors: the end of phase A's
+        // sweep (d, r, Ad) is what the 126 MB L2 still holds after the grid
+        // barrier, so at large n the first part of this pass hits L2 (and
+        // the next kernel, which walks d forwards, starts on L2 hits too):
+        // config 4 DRAM traffic 314 -> 267 MB per launch (the time is set by
+        // the loads in flight of the cooperative grid, not by DRAM bytes;
+        // a two-pair unrolled form at 2 blocks / SM measured slower)
         const int64_t n2 = g.n / 2;
         float4 *d4 = reinterpret_cast<float4 *>(b.d);
         float4 *x4 = reinterpret_cast<float4 *>(x);
         float4 *r4 = reinterpret_cast<float4 *>(b.r);
         const float4 *a4 = reinterpret_cast<const float4 *>(b.ad);
-        for (int64_t j = i0; j < n2; j += stride) {
+        for (int64_t j = n2 - 1 - i0; j >= 0; j -= stride) {
             const float4 dv = d4[j], xv = x4[j], rv = r4[j], av = a4[j];
             const float2 d0 = make_float2(dv.x, dv.y), d1 = make_float2(dv.z, dv.w);
             const float2 x0 = cadd(make_float2(xv.x, xv.y), cmul(al, d0));
@@ -703,7 +710,9 @@ __global__ void __launch_bounds__(256, XOP ? 2 : 3) k_admm_head(CgTailArgs A) {
             auto sub4 = [](float4 m, float4 e) {
                 return make_float4(m.x - e.x, m.y - e.y, m.z - e.z, m.w - e.w);
             };
-            for (int64_t j = i0; j < n2; j += stride) {
+            // backwards: the end of phase 1's sweep (mu, eta, fhd) is what
+            // L2 holds after the barrier (as the CG tail's update pass)
+            for (int64_t j = n2 - 1 - i0; j >= 0; j -= stride) {
                 int t, xx, y;
                 unflat(g, 2 * j, t, xx, y);
                 const int64_t row = (int64_t)t * g.nx;
