@@ -217,9 +217,16 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         const char *e = dbg_env("CSR_FWD_PS");
         tc.fwd_ps = tc.fwd_ts && !(e && e[0] == '0');
     }
+    // ... on CTA pairs (cta_group::2: M = 256, B split over the pair) when
+    // the sample tiles pair up within a frame; CSR_FWD_PAIR=0 keeps one CTA
+    {
+        const char *e = dbg_env("CSR_FWD_PAIR");
+        tc.fwd_pair = tc.fwd_ps && tc.mt_f % 2 == 0 && !(e && e[0] == '0');
+    }
     if (tc.fwd_ts) {
         const int NTt = tc.Nf / 256;
-        const int64_t units = mtiles * NTt;
+        const int CLp = tc.fwd_pair ? 2 : 1;
+        const int64_t units = mtiles / CLp * NTt;
         tc.fts_smem = (tc.fwd_ps ? FPS_STAGES * FPS_STAGE : FTS_STAGES * 2 * FTS_B_TILE) + 1024 + 256;
         // CTAs = SMs (persistent); pieces of a sample tile split across CTAs
         // are limited to the 4 flag slots per tile
@@ -231,14 +238,14 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
                 return b;
             };
             int mp = 1;
-            for (int64_t m = 0; m < mtiles; ++m)
+            for (int64_t m = 0; m < mtiles / CLp; ++m)
                 mp = std::max<int>(mp, (int)(owner((m + 1) * NTt - 1) - owner(m * NTt) + 1));
             return mp;
         };
-        int64_t Gc = std::min<int64_t>(148, units);
+        int64_t Gc = std::min<int64_t>(148 / CLp, units);
         int maxp = max_pieces(Gc);
-        while (maxp > 4 && Gc > mtiles) maxp = max_pieces(--Gc);
-        tc.fts_ctas = (int)Gc;
+        while (maxp > 4 && Gc > mtiles / CLp) maxp = max_pieces(--Gc);
+        tc.fts_ctas = (int)Gc * CLp;
         G = std::max(G, maxp - 1);  // kdp holds pieces 1.. (piece 0 stays in registers)
         tc.fts_pieces = maxp;
     }
@@ -382,6 +389,9 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     set_smem(k_tc_forward_ts<4, true>, tc.fts_smem);
     set_smem(k_tc_forward_ts<8, true>, tc.fts_smem);
     set_smem(k_tc_forward_ts<16, true>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<4, true, true>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<8, true, true>, tc.fts_smem);
+    set_smem(k_tc_forward_ts<16, true, true>, tc.fts_smem);
     tc.enabled = true;
     return 0;
 }
@@ -412,7 +422,7 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         P.a = a;
         P.mt_per_frame = tc.mt_f;
         P.nt_tiles = tc.Nf / 256;
-        P.units = (int64_t)tc.T * tc.mt_f * P.nt_tiles;
+        P.units = (int64_t)tc.T * tc.mt_f / (tc.fwd_pair ? 2 : 1) * P.nt_tiles;
         P.fa_hi = reinterpret_cast<const uint4 *>(tc.fa_hi);
         P.fa_lo = reinterpret_cast<const uint4 *>(tc.fa_lo);
         P.p0p = tc.p0p;
@@ -427,10 +437,12 @@ inline int tc_forward(TcPlan &tc, const float2 *img, float2 *user, cudaStream_t 
         dim3 grid((unsigned)tc.fts_ctas);
         switch (tc.Cp) {
 #define FTS_LAUNCH(CPV)                                                                        \
-    (tc.fwd_ps ? launch(k_tc_forward_ts<CPV, true>, grid, FTS_THREADS, tc.fts_smem, st,          \
-                        tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P)             \
-               : launch(k_tc_forward_ts<CPV, false>, grid, FTS_THREADS, tc.fts_smem, st,         \
-                        tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P))
+    (tc.fwd_pair ? launch_cl(k_tc_forward_ts<CPV, true, true>, grid, FTS_THREADS, tc.fts_smem,   \
+                             st, 2, tc.tm_xb128_hi, tc.tm_xb128_lo, tc.tm_fa_hi, tc.tm_fa_lo, P) \
+     : tc.fwd_ps ? launch(k_tc_forward_ts<CPV, true>, grid, FTS_THREADS, tc.fts_smem, st,        \
+                          tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P)           \
+                 : launch(k_tc_forward_ts<CPV, false>, grid, FTS_THREADS, tc.fts_smem, st,       \
+                          tc.tm_xb256_hi, tc.tm_xb256_lo, tc.tm_fa_hi, tc.tm_fa_lo, P))
             case 4: FTS_LAUNCH(4); break;
             case 8: FTS_LAUNCH(8); break;
             default: FTS_LAUNCH(16); break;

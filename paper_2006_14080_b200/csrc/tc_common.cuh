@@ -68,6 +68,7 @@ struct TcPlan {
     int nt = 1, mt_f = 1, G = 1, nt_per_group = 1, mt_a = 1, kb_total = 1, kb_per_split = 1;
     bool fwd_ts = false;  // A-stationary forward (2*nyp <= 256)
     bool fwd_ps = false;  // its PS form (A from shared memory, two accumulators)
+    bool fwd_pair = false;  // the PS form on CTA pairs (cta_group::2)
     unsigned long long *trace = nullptr;  // CSR_TRACE: per-CTA timestamps
     unsigned long long *probe = nullptr;   // [PROBE_SLOTS][4] live timing slots
     int fexp = 0, aexp = 0;               // CSR_FEXP / CSR_EXP profiling flags

@@ -308,7 +308,16 @@ __device__ __forceinline__ int fts_owner(int64_t U, int G, int64_t u) {
 // shared memory next to B in every K block (TMA, SW128) instead of held in
 // tensor memory, which frees TMEM for two 256-column accumulators: the
 // epilogue drains unit u while the MMAs of unit u+1 run.
-template <int CP, bool PS>
+// PAIR (with PS): the walk runs on CTA pairs (cta_group::2, as the SS
+// form): a unit is a pair of consecutive sample tiles x one 256-row N tile,
+// M = 256 pair MMAs, each CTA stages its 128 sample rows of A and 128 of the
+// 256 image rows of B (64 KiB stages, three of them), the leader issues.
+// Unit ranges, pieces and their flags are per pair; each CTA folds and
+// writes the rows of its own sample tile.
+constexpr int FPP_STAGES = 3;
+constexpr int FPP_STAGE = 2 * TC_A_TILE + FTS_B_TILE;  // A hi/lo + B hi/lo halves
+static_assert(FPP_STAGES * FPP_STAGE <= FPS_STAGES * FPS_STAGE, "pair stages fit");
+template <int CP, bool PS, bool PAIR = false>
 __global__ void __launch_bounds__(FTS_THREADS, 1)
     k_tc_forward_ts(const __grid_constant__ CUtensorMap tmB_hi,
                     const __grid_constant__ CUtensorMap tmB_lo,
@@ -323,9 +332,13 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     // TS: one K block = [B_hi | B_lo] x 256 rows; PS: [A_hi | A_lo | B_hi | B_lo]
-    constexpr int STAGE = PS ? FPS_STAGE : 2 * FTS_B_TILE;
-    constexpr int NSTG = PS ? FPS_STAGES : FTS_STAGES;
+    // (PAIR: B halves of 128 rows)
+    static_assert(!PAIR || PS, "the pair form stages A in shared memory");
+    constexpr int STAGE = PAIR ? FPP_STAGE : PS ? FPS_STAGE : 2 * FTS_B_TILE;
+    constexpr int NSTG = PAIR ? FPP_STAGES : PS ? FPS_STAGES : FTS_STAGES;
     constexpr int BOFF = PS ? 2 * TC_A_TILE : 0;  // B offset in a stage
+    constexpr int BH = PAIR ? FTS_B_TILE / 2 : FTS_B_TILE;  // B hi (or lo) bytes per CTA
+    constexpr int CL = PAIR ? 2 : 1;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTG * STAGE);
     uint64_t *empty = full + NSTG;
     uint64_t *tfull = empty + NSTG;     // [2] (PS: one per accumulator)
@@ -336,10 +349,15 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     __shared__ float2 part_acc[128][CP + 1];  // row sums folded across the quarters
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int G = gridDim.x;
+    // (PAIR: G pairs, this CTA's pair `pid`, units of sample-tile pairs)
+    const int G = gridDim.x / CL;
+    const int pid = blockIdx.x / CL;
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0;
     const int64_t U = P.units;
     const int NT = P.nt_tiles;
-    const int64_t u0 = fts_u0(U, G, blockIdx.x), u1 = fts_u0(U, G, blockIdx.x + 1);
+    const int64_t u0 = fts_u0(U, G, pid), u1 = fts_u0(U, G, pid + 1);
+    // sample tile (128 rows, over T * mt_per_frame) of unit-tile index m
+    auto stile = [&](int64_t m) { return PAIR ? 2 * m + crank : m; };
     const int nkb = P.a.Kf / 64;
     unsigned long long *tr = P.trace ? P.trace + (size_t)blockIdx.x * 32 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
@@ -357,17 +375,24 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 16);
+            mbar_init(&tempty[b], 16 * CL);
         }
         mbar_init(a_ready, 16);
         mbar_init(a_free, 1);
-        fence_barrier_init();
+        if (PAIR) fence_barrier_init_cluster();
+        else fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // the leader's barriers exist before any remote use
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the leader's `full` barriers (shared::cluster) for the pair's TMA loads
+    const uint32_t lead_full = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
     // A rows of sample tile m -> TMEM: the four epilogue warps of a lane
@@ -405,9 +430,16 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     if (PS && warp == 0 && lane == 0) {
         for (int i = 0; i < npre; ++i) {
             uint8_t *st = smem + i * STAGE;
-            mbar_arrive_expect_tx(&full[i], STAGE);
-            tma_load_2d(st, &tmA_hi, &full[i], i * 64, (int)(u0 / NT) * 128);
-            tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[i], i * 64, (int)(u0 / NT) * 128);
+            const int ar = (int)stile(u0 / NT) * 128;
+            if (PAIR) {
+                if (crank == 0) mbar_arrive_expect_tx(&full[i], CL * STAGE);
+                tma_load_2d_pair(st, &tmA_hi, lead_full + i * 8, i * 64, ar);
+                tma_load_2d_pair(st + TC_A_TILE, &tmA_lo, lead_full + i * 8, i * 64, ar);
+            } else {
+                mbar_arrive_expect_tx(&full[i], STAGE);
+                tma_load_2d(st, &tmA_hi, &full[i], i * 64, ar);
+                tma_load_2d(st + TC_A_TILE, &tmA_lo, &full[i], i * 64, ar);
+            }
         }
     }
 
@@ -416,6 +448,24 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     if (run) probe_enter(P.probe);
 
     if (!run) {
+        // gated off: complete the prologue's A loads (their stages expect
+        // the B bytes too) before the CTA may leave
+        if (npre > 0 && warp == 0 && lane == 0) {
+            const int64_t m = u0 / NT, ms = stile(m);
+            const int t = (int)(ms / P.mt_per_frame);
+            const int brow = t * P.a.Nf + (int)(u0 - m * NT) * 256 + (int)crank * 128;
+            for (int i = 0; i < npre; ++i) {
+                uint8_t *st = smem + i * STAGE;
+                if (PAIR) {
+                    tma_load_2d_pair(st + BOFF, &tmB_hi, lead_full + i * 8, i * 64, brow);
+                    tma_load_2d_pair(st + BOFF + BH, &tmB_lo, lead_full + i * 8, i * 64, brow);
+                } else {
+                    tma_load_2d(st + BOFF, &tmB_hi, &full[i], i * 64, brow);
+                    tma_load_2d(st + BOFF + FTS_B_TILE, &tmB_lo, &full[i], i * 64, brow);
+                }
+                if (crank == 0) mbar_wait(&full[i], 0);
+            }
+        }
     } else if (warp == 0) {
         // ---- TMA producer over the CTA's units
         if (lane == 0) {
@@ -423,13 +473,26 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             for (int64_t u = u0; u < u1; ++u) {
                 const int64_t m = u / NT;
                 const int nt = (int)(u - m * NT);
-                const int t = (int)(m / P.mt_per_frame);
-                const int brow = t * P.a.Nf + nt * 256;
-                const int arow = (int)m * 128;  // (T * Mk) rows of A, Mk per frame
+                const int64_t ms = stile(m);  // this CTA's sample tile
+                const int t = (int)(ms / P.mt_per_frame);
+                const int brow = t * P.a.Nf + nt * 256 + (int)crank * 128;
+                const int arow = (int)ms * 128;  // (T * Mk) rows of A, Mk per frame
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % NSTG;
                     const uint32_t ph = (it / NSTG) & 1;
                     uint8_t *st = smem + s * STAGE;
+                    if (PAIR) {
+                        const uint32_t fb = lead_full + s * 8;
+                        if (it >= npre) {
+                            mbar_wait(&empty[s], ph ^ 1);
+                            if (crank == 0) mbar_arrive_expect_tx(&full[s], CL * STAGE);
+                            tma_load_2d_pair(st, &tmA_hi, fb, kb * 64, arow);
+                            tma_load_2d_pair(st + TC_A_TILE, &tmA_lo, fb, kb * 64, arow);
+                        }
+                        tma_load_2d_pair(st + BOFF, &tmB_hi, fb, kb * 64, brow);
+                        tma_load_2d_pair(st + BOFF + BH, &tmB_lo, fb, kb * 64, brow);
+                        continue;
+                    }
                     if (it < npre) {  // A already in flight (prologue)
                         tma_load_2d(st + BOFF, &tmB_hi, &full[s], kb * 64, brow);
                         tma_load_2d(st + BOFF + FTS_B_TILE, &tmB_lo, &full[s], kb * 64, brow);
@@ -449,10 +512,10 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        // ---- MMA issuer: the whole warp runs the loop, one elected lane
-        // issues (FWD_ELECT)
-        if (FWD_ELECT || lane == 0) {
-            constexpr uint32_t idesc = idesc_f16(128, 256);
+        // ---- MMA issuer (the pair's leader): the whole warp runs the loop,
+        // one elected lane issues (FWD_ELECT)
+        if (crank == 0 && (FWD_ELECT || lane == 0)) {
+            constexpr uint32_t idesc = idesc_f16(128 * CL, 256);
             const uint32_t a_hi = tmem, a_lo = tmem + 128, dcol = tmem + 256;
             int it = 0, tc = 0, seg = 0;
             int64_t m_prev = -1;
@@ -485,9 +548,15 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint32_t ac = kb * 32 + kk * 8;
                             const uint64_t dbh = desc_sw128(st + BOFF + kk * 32);
-                            const uint64_t dbl = desc_sw128(st + BOFF + FTS_B_TILE + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + BOFF + BH + kk * 32);
                             if (P.exp_flags & 1) continue;
-                            if (PS) {
+                            if (PAIR) {
+                                const uint64_t dah = desc_sw128(st + kk * 32);
+                                const uint64_t dal = desc_sw128(st + TC_A_TILE + kk * 32);
+                                mma_f16_pair<1>(dacc, dah, dbh, idesc, (kb | kk) != 0);
+                                mma_f16_pair<2>(dacc, dah, dbl, idesc, 1);
+                                mma_f16_pair<0>(dacc, dal, dbh, idesc, 1);
+                            } else if (PS) {
                                 const uint64_t dah = desc_sw128(st + kk * 32);
                                 const uint64_t dal = desc_sw128(st + TC_A_TILE + kk * 32);
                                 mma_f16_fill(dacc, dah, dbh, idesc, (kb | kk) != 0);
@@ -499,11 +568,15 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                                 mma_f16_ts(dcol, a_lo + ac, dbh, idesc, 1);
                             }
                         }
-                        mma_commit(&empty[s]);
+                        if (PAIR) mma_commit_pair_mc(&empty[s], 3);
+                        else mma_commit(&empty[s]);
                     }
                     if (FWD_ELECT) __syncwarp();
                 }
-                if (fwd_one()) mma_commit(&tfull[ab]);
+                if (fwd_one()) {
+                    if (PAIR) mma_commit_pair_mc(&tfull[ab], 3);
+                    else mma_commit(&tfull[ab]);
+                }
                 if (FWD_ELECT) __syncwarp();
                 if (tr && tc < 8 && lane == 0) tr[16 + tc] = gtimer();
             }
@@ -519,17 +592,18 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
         const int64_t Mk = P.a.Mk;
         int tc = 0, seg = 0;
         for (int64_t us = u0; us < u1; ++seg) {
-            const int64_t m = us / NT;
+            const int64_t m = us / NT;            // unit tile (PAIR: tile pair)
             const int64_t ue = min(u1, (m + 1) * NT);
-            const int t = (int)(m / P.mt_per_frame);
+            const int64_t ms = stile(m);          // this CTA's sample tile
+            const int t = (int)(ms / P.mt_per_frame);
             const bool last_seg = ue == u1;
-            const int64_t kloc = (int64_t)(m % P.mt_per_frame) * 128 + row;
+            const int64_t kloc = (int64_t)(ms % P.mt_per_frame) * 128 + row;
             const bool valid = kloc < P.a.M;
             const float2 *p0row = P.p0p + ((int64_t)t * Mk + kloc) * P.a.nxp;
             const int b_first = fts_owner(U, G, m * NT);
             const int b_last = fts_owner(U, G, (m + 1) * NT - 1);
             const int npieces = b_last - b_first + 1;
-            const int piece = blockIdx.x - b_first;
+            const int piece = pid - b_first;
             const int64_t grow = (int64_t)t * Mk + kloc;
             float2 acc[CP];
 #pragma unroll
@@ -553,7 +627,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                 if (u + 1 == ue && piece == 0 && npieces > 1 && qt == 0) {
                     for (int pc = 1; pc < npieces; ++pc) {
                         unsigned f = 0;
-                        const unsigned *flag = P.tick + m * 4 + pc;
+                        const unsigned *flag = P.tick + ms * 4 + pc;
                         do {
                             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];"
                                          : "=r"(f) : "l"(flag) : "memory");
@@ -574,7 +648,10 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     if (hh == 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[ab]);
+                        if (lane == 0) {
+                            if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[ab]), 0));
+                            else mbar_arrive(&tempty[ab]);
+                        }
                     }
                     if (!(P.exp_flags & 4)) {
 #pragma unroll
@@ -612,7 +689,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     asm volatile("bar.sync 2, 128;" ::: "memory");
                     if (threadIdx.x == 64) {
                         asm volatile("st.release.gpu.global.u32 [%0], %1;"
-                                     ::"l"(P.tick + m * 4 + piece), "r"(1u) : "memory");
+                                     ::"l"(P.tick + ms * 4 + piece), "r"(1u) : "memory");
                     }
                 } else {
                     for (int pc = 1; pc < npieces; ++pc) {
@@ -623,7 +700,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     if (npieces > 1) {
                         asm volatile("bar.sync 2, 128;" ::: "memory");
                         if (threadIdx.x < 64 + npieces - 1 && threadIdx.x >= 64)
-                            P.tick[m * 4 + 1 + (threadIdx.x - 64)] = 0u;  // re-arm
+                            P.tick[ms * 4 + 1 + (threadIdx.x - 64)] = 0u;  // re-arm
                     }
                     float mx = 0.f;
 #pragma unroll
@@ -645,9 +722,13 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     }
     __syncthreads();
     if (run) probe_exit(P.probe);
+    // no CTA of a pair leaves while the leader's MMAs / commits may still
+    // touch the peer
+    if (PAIR) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if (PAIR) tmem_dealloc_pair(tmem, 512);
+        else tmem_dealloc(tmem, 512);
     }
 }
 

@@ -1,0 +1,19 @@
+#!/bin/bash
+# pair persistent forward (configs 0/1): tests first, then op timing vs the single-CTA PS form, benches
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+out=gpurun_out/r02aa_pair_ps.txt
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $out 2>&1
+echo "tests rc=$?" >> $out
+tail -3 $out
+if grep -q "tests rc=0" $out; then
+  for c in 1 0; do
+    timeout 200 python tools/time_ops.py $c >> $out 2>&1
+    CSR_VARIANT=dbg CSR_FWD_PAIR=0 timeout 200 python tools/time_ops.py $c >> $out 2>&1
+  done
+  for c in 1 0; do
+    timeout 600 python bench.py --config $c --no-cpu > gpurun_out/r02aa_bench_c$c.json 2> gpurun_out/r02aa_bench_c$c.err
+    python -c "import json;d=json.load(open('gpurun_out/r02aa_bench_c$c.json'));print($c, d['value'],d['e2e']['value'],d['roofline']['ms_per_launch'],d['roofline']['step_breakdown_ms'])" >> $out
+  done
+fi
+tail -8 $out
