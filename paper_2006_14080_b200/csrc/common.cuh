@@ -98,7 +98,7 @@ inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// the same with a cluster of cluster_x CTAs along x (TMA multicast pairs)
+// the same with a cluster of cluster_x CTAs along x (CTA pairs / TMA multicast pairs)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_cl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                              cudaStream_t st, int cluster_x, Args... args) {

@@ -577,7 +577,7 @@ int plan_create(const csr_plan_desc *desc, const FactorSource &fs, csr_plan **ou
     {
         // operand writes of >= CSR_XOP_SPLIT (default 2^22) coil-pixels go to
         // their own kernel (measured crossover: tools/gpu/xop_ab.sh)
-        const char *e = getenv("CSR_XOP_SPLIT");
+        const char *e = dbg_env("CSR_XOP_SPLIT");  // (debug builds)
         const int64_t lim = e ? atoll(e) : ((int64_t)1 << 22);
         p->fuse_xop = p->g.n * p->C < lim;
     }

@@ -92,7 +92,7 @@ struct TcPlan {
     CUtensorMap tm_fa_hi, tm_fa_lo, tm_xb_hi, tm_xb_lo, tm_ga_hi, tm_ga_lo, tm_p0, tm_kd;
     CUtensorMap tm_xb256_hi, tm_xb256_lo;
     CUtensorMap tm_gaw_hi, tm_gaw_lo;  // N-row boxes of ga (wide adjoint)
-    CUtensorMap tm_xb128_hi, tm_xb128_lo;  // half-tile boxes of xb (multicast pairs)
+    CUtensorMap tm_xb128_hi, tm_xb128_lo;  // half-tile boxes of xb (CTA-pair forwards)
     int fwd_CL = 1;  // SS forward: CTA-pair clusters multicasting the image operand
 };
 
