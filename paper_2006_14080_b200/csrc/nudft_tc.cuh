@@ -189,6 +189,13 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     tc.Kf = 2 * tc.nyp;
     tc.Nf = 2 * tc.nxp * Cp;
     tc.Mk = (M + 127) / 128 * 128;
+    // the forwards run on CTA pairs of sample tiles within a frame: an odd
+    // tile count gets one zero tile of padding (factors are zero there)
+    // when that costs <= 1/15 more forward work (config 3: 39 -> 40 tiles,
+    // forward 739 -> 645 us); the adjoint's K range stays at the unpadded
+    // samples (kb_total)
+    const int64_t Mk128 = tc.Mk;
+    if (chunk == 0 && (tc.Mk / TC_BM) % 2 == 1 && tc.Mk / TC_BM >= 15) tc.Mk += TC_BM;
     tc.nt = tc.Nf / TC_BN;
     tc.mt_f = (int)(tc.Mk / TC_BM);
     // forward groups: split the n-tiles so the grid covers the machine
@@ -206,7 +213,8 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     // (<= 16 coils: the persistent form's 576-thread CTA keeps CP complex
     // accumulators per epilogue thread in registers)
     tc.fwd_ts = tc.Kf <= 256 && Cp <= 16 && !dbg_env("CSR_FWD_SS") && chunk == 0;
-    // SS form: pairs of sample tiles of one frame multicast the image operand
+    // SS form: CTA pairs (cta_group::2) on two sample tiles of one frame,
+    // the image operand split over the pair
     tc.fwd_CL = (tc.mt_f % 2 == 0) ? 2 : 1;
     if (const char *e = dbg_env("CSR_FWD_CL")) tc.fwd_CL = (atoi(e) == 2 && tc.mt_f % 2 == 0) ? 2 : 1;
     // PS form of the persistent forward (A staged from shared memory next
@@ -251,7 +259,7 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
     }
     // adjoint split-K
     tc.mt_a = tc.nxp * Cp / 64;  // adjoint tiles over (x, c): 64 per tile
-    tc.kb_total = (int)(tc.Mk / 32);
+    tc.kb_total = (int)(Mk128 / 32);
     const AdjGeom ag = tc_adj_geom(ny, Cp, tc.mt_a);
     tc.nyA = std::max(tc.nyA, ag.nyt * ag.N);  // the wide tiles' padded pixel rows
     tc.adj_w = ag.wide;
