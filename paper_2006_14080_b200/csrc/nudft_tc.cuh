@@ -107,7 +107,7 @@ inline int tc_split_model(int64_t tiles, int kb_total, int64_t pix_bytes, int bl
 struct AdjGeom {
     bool wide = false;
     int N = 128, nyt = 1, NA = 4, NB = 0, chain = TC_MAX_CHAIN, blk_cycles = 768;
-    int CL = 1;  // wide kernel: CTA pairs along x sharing B by TMA multicast
+    int CL = 1;  // wide kernel: CTA pairs (cta_group::2) along x splitting B
 };
 inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     AdjGeom g;
@@ -118,23 +118,25 @@ inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     // a multiple of 32: each of the two epilogue warps of a lane quarter
     // drains (N - 128) / 2 columns >= 128 in 16-column loads
     g.N = ((ny + g.nyt - 1) / g.nyt + 31) / 32 * 32;
-    // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128)
-    g.NA = std::min(4, (512 - g.N - (g.N - 128)) / 64);
+    // pairs of x tiles (cta_group::2) split the B rows: half the rows each, a
+    // multiple of 8 (one swizzle atom)
+    g.CL = (mt_a % 2 == 0 && (g.N / 2) % 8 == 0) ? 2 : 1;
+    if (const char *e = dbg_env("CSR_ADJW_CL")) g.CL = (atoi(e) == 2 && mt_a % 2 == 0) ? 2 : 1;
+    // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128;
+    // the pair form keeps those sums in shared memory)
+    g.NA = std::min(4, (512 - g.N - (g.CL == 2 ? 0 : g.N - 128)) / 64);
     // B ring: two stages (the MMAs take ~1.3 us per K block, an L2-hit TMA
     // refill ~1 us); the rest of shared memory deepens the input ring, whose
     // TMA -> prep -> generator -> release round trip bounds the kernel with
     // two stages (measured: the skeleton without math or MMAs ran at 0.66 us
     // per K block with NB = 3, NR = 2).  The combine's sums reuse both rings.
-    g.NB = 2;
+    g.NB = g.CL == 2 ? 3 : 2;  // (pair: half-size stages)
     if (const char *e = dbg_env("CSR_ADJW_NB")) g.NB = std::max(2, std::min(4, atoi(e)));
     // three N-wide MMAs per K step truncate into one fp32 accumulator:
     // shorter chains than the two-accumulator kernel
     g.chain = TC_ADJW_CHAIN;
     if (const char *e = dbg_env("CSR_ADJW_CHAIN")) g.chain = std::max(1, atoi(e));
     g.blk_cycles = 4 * 3 * (g.N / 2 + 32);
-    // pairs of x tiles multicast the B tiles (half the rows each: a multiple of 8)
-    g.CL = (mt_a % 2 == 0 && (g.N / 2) % 8 == 0) ? 2 : 1;
-    if (const char *e = dbg_env("CSR_ADJW_CL")) g.CL = (atoi(e) == 2 && mt_a % 2 == 0) ? 2 : 1;
     return g;
 }
 
@@ -291,11 +293,12 @@ inline int tc_plan_build(TcPlan &tc, int T, int nx, int ny, int C, int64_t M,
         tc.adj_smem = fixed + tc.adj_nraw * tc.adj_stage;
     }
     if (tc.adj_w) {
-        const int fixed = tc.adjw_NB * adjw_b_stage(tc.adjw_N) + 1024 + 512;
+        const int sbytes = adjw_s_bytes(tc.adjw_N, tc.adjw_CL);
+        const int fixed = sbytes + tc.adjw_NB * adjw_b_stage(tc.adjw_N, tc.adjw_CL) + 1024 + 512;
         tc.adjw_nraw = std::min(ADJ_MAX_RAW, (227 * 1024 - fixed) / tc.adj_stage);
         tc.adjw_smem = fixed + tc.adjw_nraw * tc.adj_stage;
         // the combine's sums [N][ADJ_SUM_LD] floats over the B and input rings
-        const int rings = fixed - 1536 + tc.adjw_nraw * tc.adj_stage;
+        const int rings = fixed - 1536 - sbytes + tc.adjw_nraw * tc.adj_stage;
         if (tc.adjw_nraw < 2 || tc.adjw_N * ADJ_SUM_LD * 4 > rings) {
             tc.adj_w = false;  // keep the narrow kernel (128-row tiles)
             tc.nyA = (ny + 127) / 128 * 128;

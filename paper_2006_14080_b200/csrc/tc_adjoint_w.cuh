@@ -23,12 +23,20 @@
 // issuer (elected lane); 2-3 input prep (d'); 4-7 generators (one per TMEM
 // lane quarter, 32 samples each); 8-15 epilogue (two per lane quarter).
 //
-// CL = 2: CTA pairs along x (a cluster of two x tiles of the same frame,
-// y tile and k range) share the static B tiles: each CTA fetches half of
-// the N rows and multicasts them to both, so the L2 -> SM traffic of the
-// dominant operand halves.  A B stage is refilled only after the MMAs of
-// BOTH CTAs released it (the MMA commit is multicast to the pair's
-// bempty barriers, which count CL arrivals).
+// CL = 2: a CTA pair (cta_group::2) on two x tiles of the same frame, y
+// tile and k range: M = 256 pair MMAs (each CTA's generated A in its own
+// TMEM), the static B tiles split over the pair along N (each CTA's shared
+// memory holds N/2 of the rows), so the B traffic into each SM's shared
+// memory (TMA writes and MMA reads) halves.  The leader (rank 0) issues the
+// MMAs once both CTAs' generators filled the A stage: the peer's
+// generators arrive on their own `gen`, the peer's idle MMA warp relays
+// that to the leader's `genp` (one remote arrive per K block, off the
+// generators' path); both CTAs' B loads complete on the leader's `bfull`
+// (cta_group::2 TMA); MMA commits are multicast onto both CTAs' `bempty`,
+// `aempty` and `acc_full`; both epilogues release the accumulator on the
+// leader's `acc_empty`.  The running sums of columns >= 128 live in shared
+// memory (freed by the halved B stages), which leaves TMEM to the
+// accumulator and four A stages.
 #pragma once
 
 #include "tc_adjoint.cuh"
@@ -68,7 +76,11 @@ struct AdjWParams {
 
 // shared memory: B ring NB x (hi N x 128 B | lo N x 128 B), input ring,
 // barriers; the coil-combine sums [N][ADJ_SUM_LD] floats reuse the B ring
-__host__ __device__ constexpr int adjw_b_stage(int N) { return 2 * N * 128; }
+// (per CTA: a pair holds N/2 rows each)
+__host__ __device__ constexpr int adjw_b_stage(int N, int CL = 1) { return 2 * (N / CL) * 128; }
+// pair form: fp32 running sums of columns >= 128, [col / 4][lane] float4,
+// ahead of the B ring
+__host__ __device__ constexpr int adjw_s_bytes(int N, int CL) { return CL > 1 ? (N - 128) * 128 * 4 : 0; }
 
 template <int CP, int CL>
 __global__ void __launch_bounds__(ADJW_THREADS, 1)
@@ -83,9 +95,12 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     constexpr int OFF_D = 32 * XS * 8, OFF_DP = OFF_D + 32 * CP * 8;
     constexpr int GW = 4, SPW = 32;  // generator warps, samples per warp and K block
     const int N = P.N, NA = P.NA, NB = P.NB;
-    const int BST = adjw_b_stage(N);
+    constexpr bool PAIR = CL > 1;
+    const int BST = adjw_b_stage(N, CL);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = align1024(smem_raw);
+    uint8_t *smem_all = align1024(smem_raw);
+    float *s_run = reinterpret_cast<float *>(smem_all);  // PAIR: running sums [col][lane]
+    uint8_t *smem = smem_all + adjw_s_bytes(N, CL);      // B ring
     uint8_t *in_base = smem + NB * BST;
     float *sum_s = reinterpret_cast<float *>(smem);  // after the main loop
     uint64_t *bfull = reinterpret_cast<uint64_t *>(in_base + P.n_raw * IN_STAGE);
@@ -97,7 +112,8 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     uint64_t *rempty = dfull + ADJ_MAX_RAW;
     uint64_t *acc_full = rempty + ADJ_MAX_RAW;
     uint64_t *acc_empty = acc_full + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+    uint64_t *genp = acc_empty + 1;    // [NA] (PAIR, leader) the peer's stage written
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(genp + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x, nt = blockIdx.y;
@@ -116,11 +132,12 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         tma_prefetch(&tmKd);
         for (int s = 0; s < NB; ++s) {
             mbar_init(&bfull[s], 1);
-            mbar_init(&bempty[s], CL);
+            mbar_init(&bempty[s], 1);
         }
         for (int s = 0; s < NA; ++s) {
             mbar_init(&gen[s], GW);
             mbar_init(&aempty[s], 1);
+            mbar_init(&genp[s], 1);
         }
         for (int r = 0; r < NR; ++r) {
             mbar_init(&rfull[r], 1);
@@ -128,26 +145,35 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             mbar_init(&rempty[r], GW);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, ADJW_EW);
-        fence_barrier_init();
+        mbar_init(acc_empty, ADJW_EW * CL);
+        if (PAIR) fence_barrier_init_cluster();
+        else fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
-    if (CL > 1) cluster_sync();  // the peer's barriers exist before any multicast
+    if (PAIR) cluster_sync();  // the leader's barriers exist before any remote use
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
-    const int hrows = N / CL;  // B rows this CTA fetches (and multicasts)
+    const int hrows = N / CL;  // B rows in this CTA's shared memory
+    // the leader's barriers (shared::cluster addresses) for the pair form
+    const uint32_t lead = PAIR ? mapa_shared(smem_u32(bfull), 0) : 0;
+    auto cl_bar = [&](uint64_t *b) { return lead + (uint32_t)((uint8_t *)b - (uint8_t *)bfull); };
     auto load_b = [&](uint8_t *st, uint64_t *bar, int kb, int brow) {
-        mbar_arrive_expect_tx(bar, BST);
-        if (CL == 1) {
+        if (!PAIR) {
+            mbar_arrive_expect_tx(bar, BST);
             tma_load_2d(st, &tmB_hi, bar, kb * 64, brow);
             tma_load_2d(st + N * 128, &tmB_lo, bar, kb * 64, brow);
         } else {
+            // the leader arms its barrier for both CTAs' bytes
+            if (crank == 0) mbar_arrive_expect_tx(bar, CL * BST);
             const int o = (int)crank * hrows;
-            tma_load_2d_mc(st + o * 128, &tmB_hi, bar, kb * 64, brow + o, (1u << CL) - 1);
-            tma_load_2d_mc(st + (N + o) * 128, &tmB_lo, bar, kb * 64, brow + o, (1u << CL) - 1);
+            tma_load_2d_pair(st, &tmB_hi, cl_bar(bar), kb * 64, brow + o);
+            tma_load_2d_pair(st + hrows * 128, &tmB_lo, cl_bar(bar), kb * 64, brow + o);
         }
     };
     const uint32_t a_col0 = (uint32_t)N;                 // A stages
@@ -162,7 +188,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     if (run) probe_enter(P.probe);
 
     if (!run) {
-        if (warp == 0 && lane == 0)
+        if (warp == 0 && lane == 0 && crank == 0)
             for (int i = 0; i < pre; ++i) mbar_wait(&bfull[i], 0);
     } else if (warp == 0) {
         if (lane == 0) {
@@ -207,9 +233,17 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                 rph ^= 1;
             }
         }
+    } else if (warp == 1 && PAIR && crank != 0) {
+        // the peer's MMA warp relays "A stage written" to the leader
+        if (lane == 0)
+            for (int i = 0; i < nkb; ++i) {
+                const int sa = i % NA;
+                wait_fast(&gen[sa], (i / NA) & 1);
+                mbar_arrive_cluster(cl_bar(&genp[sa]));
+            }
     } else if (warp == 1) {
         // MMA issuer: three N-wide MMAs per K step into the one accumulator
-        const uint32_t idesc = idesc_f16(128, N);
+        const uint32_t idesc = idesc_f16(128 * CL, N);
         int i = 0;
         for (int ch = 0; ch < nchain; ++ch) {
             wait_fast(acc_empty, (ch & 1) ^ 1);
@@ -218,6 +252,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             for (int i0 = i; i < iend; ++i) {
                 const int sa = i % NA, sb = i % NB;
                 wait_fast(&gen[sa], (i / NA) & 1);
+                if (PAIR) wait_fast(&genp[sa], (i / NA) & 1);
                 ADJW_TL(i, 0, lane == 0);
                 wait_fast(&bfull[sb], (i / NB) & 1);
                 ADJW_TL(i, 1, lane == 0);
@@ -229,20 +264,33 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t dbh = desc_sw128(st + kk * 32);
-                            const uint64_t dbl = desc_sw128(st + N * 128 + kk * 32);
+                            const uint64_t dbl = desc_sw128(st + hrows * 128 + kk * 32);
                             const uint32_t acc = (i != i0) || (kk != 0);
-                            mma_f16_ts(tmem, a_hi + 8 * kk, dbh, idesc, acc);
-                            mma_f16_ts(tmem, a_hi + 8 * kk, dbl, idesc, 1);
-                            mma_f16_ts(tmem, a_lo + 8 * kk, dbh, idesc, 1);
+                            if (PAIR) {
+                                mma_f16_ts_pair(tmem, a_hi + 8 * kk, dbh, idesc, acc);
+                                mma_f16_ts_pair(tmem, a_hi + 8 * kk, dbl, idesc, 1);
+                                mma_f16_ts_pair(tmem, a_lo + 8 * kk, dbh, idesc, 1);
+                            } else {
+                                mma_f16_ts(tmem, a_hi + 8 * kk, dbh, idesc, acc);
+                                mma_f16_ts(tmem, a_hi + 8 * kk, dbl, idesc, 1);
+                                mma_f16_ts(tmem, a_lo + 8 * kk, dbh, idesc, 1);
+                            }
                         }
                     }
-                    if (CL > 1) mma_commit_mc(&bempty[sb], (uint16_t)((1u << CL) - 1));
-                    else mma_commit(&bempty[sb]);
-                    mma_commit(&aempty[sa]);
+                    if (PAIR) {
+                        mma_commit_pair_mc(&bempty[sb], (uint16_t)((1u << CL) - 1));
+                        mma_commit_pair_mc(&aempty[sa], (uint16_t)((1u << CL) - 1));
+                    } else {
+                        mma_commit(&bempty[sb]);
+                        mma_commit(&aempty[sa]);
+                    }
                 }
                 __syncwarp();
             }
-            if (elect_one()) mma_commit(acc_full);
+            if (elect_one()) {
+                if (PAIR) mma_commit_pair_mc(acc_full, (uint16_t)((1u << CL) - 1));
+                else mma_commit(acc_full);
+            }
             __syncwarp();
         }
     } else if (warp >= 4 && warp < 4 + GW) {
@@ -316,6 +364,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         const uint32_t dlo = lane_base + 64 * eh;                 // this warp's y < 128
         const uint32_t dhi = lane_base + 128 + U2 * eh;           // its y >= 128
         const uint32_t shi = lane_base + s_col0 + U2 * eh;        // their running sums
+        const int m_epi = q * 32 + lane;                          // (PAIR: smem sums)
 #pragma unroll
         for (int y = 0; y < 64; ++y) sum[y] = 0.f;
         for (int ch = 0; ch < nchain; ++ch) {
@@ -333,21 +382,42 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             for (int cb = 0; cb < U2; cb += 16) {
                 uint32_t r[16], sv[16];
                 tmem_ld16(dhi + cb, r);
-                if (ch > 0) tmem_ld16(shi + cb, sv);
+                if (!PAIR && ch > 0) tmem_ld16(shi + cb, sv);
+                // (PAIR: the shared-memory sums, [col / 4][lane] float4,
+                // fetched while the TMEM load is in flight)
+                float4 *s4 = reinterpret_cast<float4 *>(s_run) + (size_t)((U2 * eh + cb) >> 2) * 128 + m_epi;
+                float4 o[4];
+                if (PAIR) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        o[j] = ch > 0 ? s4[j * 128] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 tmem_ld_wait();
                 if (cb + 16 >= U2) {  // this warp has read its accumulator columns
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(acc_empty);
+                    if (lane == 0) {
+                        if (PAIR) mbar_arrive_cluster(cl_bar(acc_empty));
+                        else mbar_arrive(acc_empty);
+                    }
                     ADJW_TL(ch * chain, 7, lane == 0 && warp == 4 + GW);
                 }
+                if (PAIR) {
 #pragma unroll
-                for (int yy = 0; yy < 16; ++yy)
-                    sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
-                                             __uint_as_float(r[yy]));
-                tmem_st16(shi + cb, sv);
+                    for (int j = 0; j < 4; ++j)
+                        s4[j * 128] = make_float4(o[j].x + __uint_as_float(r[4 * j]),
+                                                  o[j].y + __uint_as_float(r[4 * j + 1]),
+                                                  o[j].z + __uint_as_float(r[4 * j + 2]),
+                                                  o[j].w + __uint_as_float(r[4 * j + 3]));
+                } else {
+#pragma unroll
+                    for (int yy = 0; yy < 16; ++yy)
+                        sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
+                                                 __uint_as_float(r[yy]));
+                    tmem_st16(shi + cb, sv);
+                }
             }
-            tmem_st_wait();
+            if (!PAIR) tmem_st_wait();
         }
     }
     __syncthreads();  // all MMAs and TMA loads are done: the rings are free
@@ -360,8 +430,21 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         tc_fence_after();
         for (int cb = 0; cb < U2; cb += 16) {
             uint32_t sv[16];
-            tmem_ld16(shi + cb, sv);
-            tmem_ld_wait();
+            if (PAIR) {
+                const float4 *s4 = reinterpret_cast<const float4 *>(s_run) +
+                                   (size_t)((U2 * eh + cb) >> 2) * 128 + m;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 v = s4[j * 128];
+                    sv[4 * j] = __float_as_uint(v.x);
+                    sv[4 * j + 1] = __float_as_uint(v.y);
+                    sv[4 * j + 2] = __float_as_uint(v.z);
+                    sv[4 * j + 3] = __float_as_uint(v.w);
+                }
+            } else {
+                tmem_ld16(shi + cb, sv);
+                tmem_ld_wait();
+            }
 #pragma unroll
             for (int yy = 0; yy < 16; ++yy)
                 sum_s[(128 + U2 * eh + cb + yy) * ADJ_SUM_LD + m] = __uint_as_float(sv[yy]);
@@ -395,12 +478,13 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     }
     __syncthreads();
     if (run) probe_exit(P.probe);
-    // no CTA of a pair leaves while the peer's MMA commits may still
-    // arrive on its barriers
-    if (CL > 1) cluster_sync();
+    // no CTA of a pair leaves while the leader's MMAs / commits may still
+    // touch the peer (its shared memory, barriers and tensor memory)
+    if (PAIR) cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if (PAIR) tmem_dealloc_pair(tmem, 512);
+        else tmem_dealloc(tmem, 512);
     }
 }
 
