@@ -133,8 +133,12 @@ inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     g.NB = g.CL == 2 ? 3 : 2;  // (pair: half-size stages)
     if (const char *e = dbg_env("CSR_ADJW_NB")) g.NB = std::max(2, std::min(4, atoi(e)));
     // three N-wide MMAs per K step truncate into one fp32 accumulator:
-    // shorter chains than the two-accumulator kernel
-    g.chain = TC_ADJW_CHAIN;
+    // shorter chains than the two-accumulator kernel.  The error grows
+    // linearly with the chain (config 4 adjoint rel-L2 2.8e-6 at 12, 3.7e-6
+    // at 16, 5.5e-6 at 24; tolerance 1e-5); the pair form at N = 256 drains
+    // ~3200 cycles per chain with the MMAs stalled, so it takes chains of 16
+    // (config 4 12.66 -> 12.31 ms, profiles/r02al_pair_drain.txt)
+    g.chain = (g.CL == 2 && g.N >= 256) ? 16 : TC_ADJW_CHAIN;
     if (const char *e = dbg_env("CSR_ADJW_CHAIN")) g.chain = std::max(1, atoi(e));
     g.blk_cycles = 4 * 3 * (g.N / 2 + 32);
     return g;

@@ -371,6 +371,44 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             wait_slow(acc_full, ch & 1);
             ADJW_TL(ch * chain, 6, lane == 0 && warp == 4 + GW);
             tc_fence_after();
+            if (PAIR) {
+                // fewer TMEM round trips: each wait covers 16 columns of the
+                // register-summed half and 16 of the shared-memory-summed ones
+                const int nc = U2 / 16;  // 16-column chunks >= 128 (1 .. 4)
+                float4 *s4b = reinterpret_cast<float4 *>(s_run) + (size_t)((U2 * eh) >> 2) * 128 + m_epi;
+                auto rmw16 = [&](int c, const uint32_t (&r2)[16]) {
+                    float4 *s4 = s4b + (size_t)c * 4 * 128;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float4 o = ch > 0 ? s4[j * 128] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        s4[j * 128] = make_float4(o.x + __uint_as_float(r2[4 * j]),
+                                                  o.y + __uint_as_float(r2[4 * j + 1]),
+                                                  o.z + __uint_as_float(r2[4 * j + 2]),
+                                                  o.w + __uint_as_float(r2[4 * j + 3]));
+                    }
+                };
+                auto release = [&]() {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(cl_bar(acc_empty));
+                    ADJW_TL(ch * chain, 7, lane == 0 && warp == 4 + GW);
+                };
+                // four rounds: 16 register-summed columns + 16 shared-memory-
+                // summed columns per TMEM wait (nc <= 4)
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    uint32_t r[16], r2[16];
+                    tmem_ld16(dlo + rr * 16, r);
+                    const bool hc = rr < nc;
+                    if (hc) tmem_ld16(dhi + rr * 16, r2);
+                    tmem_ld_wait();
+                    if (rr == 3) release();
+#pragma unroll
+                    for (int yy = 0; yy < 16; ++yy) sum[rr * 16 + yy] += __uint_as_float(r[yy]);
+                    if (hc) rmw16(rr, r2);
+                }
+                continue;
+            }
 #pragma unroll
             for (int cb = 0; cb < 2; ++cb) {
                 uint32_t r[32];
