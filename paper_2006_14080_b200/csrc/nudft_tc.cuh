@@ -125,6 +125,7 @@ inline AdjGeom tc_adj_geom(int ny, int Cp, int mt_a = 0) {
     // TMEM: D (N) + A stages (64 each) + sums of columns >= 128 (N - 128;
     // the pair form keeps those sums in shared memory)
     g.NA = std::min(4, (512 - g.N - (g.CL == 2 ? 0 : g.N - 128)) / 64);
+    if (const char *e = dbg_env("CSR_ADJW_NA")) g.NA = std::max(2, std::min(g.NA, atoi(e)));
     // B ring: two stages (the MMAs take ~1.3 us per K block, an L2-hit TMA
     // refill ~1 us); the rest of shared memory deepens the input ring, whose
     // TMA -> prep -> generator -> release round trip bounds the kernel with

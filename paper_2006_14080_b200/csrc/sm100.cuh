@@ -224,6 +224,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
+// the same without release semantics (no cluster-scope fence of the
+// thread's prior memory operations): for relaying an arrival whose ordering
+// the relaying thread has already acquired from a CTA-local barrier on
+// tcgen05 operations that completed (tcgen05.wait::ld / wait::st)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init_cluster() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
     uint64_t *acc_full = rempty + ADJ_MAX_RAW;
     uint64_t *acc_empty = acc_full + 1;
     uint64_t *genp = acc_empty + 1;    // [NA] (PAIR, leader) the peer's stage written
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(genp + 4);
+    uint64_t *acc_emptyp = genp + 4;   // (PAIR, leader) the peer's drain done
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_emptyp + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x, nt = blockIdx.y;
@@ -139,13 +140,14 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             mbar_init(&aempty[s], 1);
             mbar_init(&genp[s], 1);
         }
+        mbar_init(acc_emptyp, 1);
         for (int r = 0; r < NR; ++r) {
             mbar_init(&rfull[r], 1);
             mbar_init(&dfull[r], 2);
             mbar_init(&rempty[r], GW);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, ADJW_EW * CL);
+        mbar_init(acc_empty, ADJW_EW);
         if (PAIR) fence_barrier_init_cluster();
         else fence_barrier_init();
     }
@@ -234,12 +236,21 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             }
         }
     } else if (warp == 1 && PAIR && crank != 0) {
-        // the peer's MMA warp relays "A stage written" to the leader
+        // the peer's MMA warp relays "A stage written" and "accumulator
+        // drained" to the leader: it acquires the CTA-local barrier (the
+        // generators' tcgen05.st / the epilogue's tcgen05.ld have completed
+        // before their local arrive) and forwards it with a relaxed
+        // cluster-scope arrive (a release.cluster arrive costs ~1900-2800
+        // cycles, measured: on the drain it stalled every chain end)
         if (lane == 0)
             for (int i = 0; i < nkb; ++i) {
+                if (i > 0 && i % chain == 0) {
+                    wait_fast(acc_empty, (i / chain - 1) & 1);
+                    mbar_arrive_cluster_relaxed(cl_bar(acc_emptyp));
+                }
                 const int sa = i % NA;
                 wait_fast(&gen[sa], (i / NA) & 1);
-                mbar_arrive_cluster(cl_bar(&genp[sa]));
+                mbar_arrive_cluster_relaxed(cl_bar(&genp[sa]));
             }
     } else if (warp == 1) {
         // MMA issuer: three N-wide MMAs per K step into the one accumulator
@@ -247,6 +258,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
         int i = 0;
         for (int ch = 0; ch < nchain; ++ch) {
             wait_fast(acc_empty, (ch & 1) ^ 1);
+            if (PAIR) wait_fast(acc_emptyp, (ch & 1) ^ 1);
             tc_fence_after();
             const int iend = min(nkb, i + chain);
             for (int i0 = i; i < iend; ++i) {
@@ -387,10 +399,10 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                                                   o.w + __uint_as_float(r2[4 * j + 3]));
                     }
                 };
-                auto release = [&]() {
+                auto release = [&]() {  // (local: the peer's is relayed)
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(cl_bar(acc_empty));
+                    if (lane == 0) mbar_arrive(acc_empty);
                     ADJW_TL(ch * chain, 7, lane == 0 && warp == 4 + GW);
                 };
                 // four rounds: 16 register-summed columns + 16 shared-memory-
@@ -402,6 +414,7 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
                     const bool hc = rr < nc;
                     if (hc) tmem_ld16(dhi + rr * 16, r2);
                     tmem_ld_wait();
+                    ADJW_TL(600 + ch, rr, lane == 0 && warp == 4 + GW);
                     if (rr == 3) release();
 #pragma unroll
                     for (int yy = 0; yy < 16; ++yy) sum[rr * 16 + yy] += __uint_as_float(r[yy]);
@@ -420,42 +433,21 @@ __global__ void __launch_bounds__(ADJW_THREADS, 1)
             for (int cb = 0; cb < U2; cb += 16) {
                 uint32_t r[16], sv[16];
                 tmem_ld16(dhi + cb, r);
-                if (!PAIR && ch > 0) tmem_ld16(shi + cb, sv);
-                // (PAIR: the shared-memory sums, [col / 4][lane] float4,
-                // fetched while the TMEM load is in flight)
-                float4 *s4 = reinterpret_cast<float4 *>(s_run) + (size_t)((U2 * eh + cb) >> 2) * 128 + m_epi;
-                float4 o[4];
-                if (PAIR) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        o[j] = ch > 0 ? s4[j * 128] : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
+                if (ch > 0) tmem_ld16(shi + cb, sv);
                 tmem_ld_wait();
                 if (cb + 16 >= U2) {  // this warp has read its accumulator columns
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        if (PAIR) mbar_arrive_cluster(cl_bar(acc_empty));
-                        else mbar_arrive(acc_empty);
-                    }
+                    if (lane == 0) mbar_arrive(acc_empty);
                     ADJW_TL(ch * chain, 7, lane == 0 && warp == 4 + GW);
                 }
-                if (PAIR) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        s4[j * 128] = make_float4(o[j].x + __uint_as_float(r[4 * j]),
-                                                  o[j].y + __uint_as_float(r[4 * j + 1]),
-                                                  o[j].z + __uint_as_float(r[4 * j + 2]),
-                                                  o[j].w + __uint_as_float(r[4 * j + 3]));
-                } else {
-#pragma unroll
-                    for (int yy = 0; yy < 16; ++yy)
-                        sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
-                                                 __uint_as_float(r[yy]));
-                    tmem_st16(shi + cb, sv);
-                }
+                for (int yy = 0; yy < 16; ++yy)
+                    sv[yy] = __float_as_uint((ch > 0 ? __uint_as_float(sv[yy]) : 0.f) +
+                                             __uint_as_float(r[yy]));
+                tmem_st16(shi + cb, sv);
             }
-            if (!PAIR) tmem_st_wait();
+            tmem_st_wait();
         }
     }
     __syncthreads();  // all MMAs and TMA loads are done: the rings are free

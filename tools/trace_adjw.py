@@ -64,7 +64,25 @@ ch = [(i, t[i, 6], t[i, 7]) for i in range(n) if t[i, 6] > 0]
 if ch:
     drains = [c[2] - c[1] for c in ch if c[2] > 0]
     print("chains", len(ch), "drain (acc_full seen -> acc_empty)", np.median(drains), "cycles")
-    # MMA restart after a chain: issue of the chain's first block vs the previous release
-    for (i, full, empty) in ch[1:4]:
-        print(f"  chain at kb {i}: release {empty - t0}, next issue {issue[i] - t0 if i < n else -1},"
-              f" previous issue {issue[i - 1] - t0}")
+    # chain ch's end: the epilogue's acc_full seen / release stamps are in row
+    # ch * L (slot 6 / 7); the MMAs of block (ch + 1) * L wait for that release
+    L = ch[1][0] - ch[0][0] if len(ch) > 1 else n
+    stall, after = [], []
+    for (i, full, empty) in ch[:-1]:
+        nb = i + L
+        if nb < n and empty > 0:
+            stall.append(issue[nb] - issue[nb - 1])
+            after.append(issue[nb] - empty)
+    if stall:
+        print(f"chain {L}: MMA gap at a chain end (issue of its first block after the previous one)",
+              np.median(stall), "cycles; of it after the local release", np.median(after))
+
+# drain rounds (rows 600 + chain, slots 0..3: each TMEM round's wait done)
+dr = buf[65536 + 8 * 600: 65536 + 8 * 1024].reshape(-1, 8).astype(np.int64)
+rows = [r for r in range(dr.shape[0]) if dr[r, 0] > 0]
+if rows and ch:
+    seen = {c: f for (c, f, e) in [(i // max(L, 1), full, empty) for (i, full, empty) in ch]}
+    d = [[dr[r, 0] - seen.get(r, dr[r, 0])] + list(np.diff(dr[r, :4])) for r in rows if r in seen]
+    if d:
+        print("drain rounds (cycles: acc_full seen -> round 0 done, then per round):",
+              np.median(np.array(d), axis=0))
