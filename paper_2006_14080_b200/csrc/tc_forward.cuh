@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
     uint64_t *empty = full + NSTG;
     uint64_t *tfull = empty + NSTG;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *tempty_p = tempty + 2;  // (PAIR, leader) the peer's accumulator drains
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty_p + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mtile = blockIdx.x;
@@ -82,7 +83,8 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4 * CL);
+            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty_p[i], 1);
         }
         if (PAIR) fence_barrier_init_cluster();
         else fence_barrier_init();
@@ -136,6 +138,18 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             }
         }
     } else if (warp == 1) {
+        if (PAIR && crank != 0 && lane == 0) {
+            // the peer's idle MMA lane relays its epilogue's accumulator
+            // releases to the leader (relaxed cluster arrive, see
+            // tc_adjoint_w.cuh: a release.cluster arrive costs ~2000 cycles)
+            const uint32_t lead_tp = mapa_shared(smem_u32(tempty_p), 0);
+            int tc = 0;
+            for (int nt = nt0; nt < nt1; ++nt, ++tc) {
+                const int ab = tc & 1;
+                mbar_wait(&tempty[ab], (tc >> 1) & 1);
+                mbar_arrive_cluster_relaxed(lead_tp + ab * 8);
+            }
+        }
         // MMA issue: lane 0 of the (leader) CTA
         if (lane == 0 && crank == 0) {
             constexpr uint32_t idesc = idesc_f16(TC_BM * CL, TC_BN);
@@ -144,6 +158,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
                 const int ab = tc & 1;
                 const uint32_t aph = (tc >> 1) & 1;
                 mbar_wait(&tempty[ab], aph ^ 1);
+                if (PAIR) mbar_wait(&tempty_p[ab], aph ^ 1);
                 tc_fence_after();
                 const uint32_t dcol = tmem + ab * TC_BN;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -219,10 +234,7 @@ __global__ void __launch_bounds__(TC_FWD_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[ab]), 0));
-                else mbar_arrive(&tempty[ab]);
-            }
+            if (lane == 0) mbar_arrive(&tempty[ab]);  // (PAIR: the peer's is relayed)
         }
         if (P.amax) {  // max|kd| for the adjoint's operand scale (order-free)
             float mx = 0.f;
@@ -345,7 +357,8 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
     uint64_t *tempty = tfull + 2;       // [2]
     uint64_t *a_ready = tempty + 2;
     uint64_t *a_free = a_ready + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_free + 1);
+    uint64_t *tempty_p = a_free + 1;    // [2] (PAIR, leader) the peer's drains
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty_p + 2);
     __shared__ float2 part_acc[128][CP + 1];  // row sums folded across the quarters
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -375,7 +388,8 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 16 * CL);
+            mbar_init(&tempty[b], 16);
+            mbar_init(&tempty_p[b], 1);
         }
         mbar_init(a_ready, 16);
         mbar_init(a_free, 1);
@@ -512,6 +526,17 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
             }
         }
     } else if (warp == 1) {
+        if (PAIR && crank != 0 && lane == 0) {
+            // the peer's idle MMA lane relays its epilogue's accumulator
+            // releases to the leader (relaxed cluster arrive)
+            const uint32_t lead_tp = mapa_shared(smem_u32(tempty_p), 0);
+            int tc = 0;
+            for (int64_t u = u0; u < u1; ++u, ++tc) {
+                const int ab = tc & 1;
+                mbar_wait(&tempty[ab], (tc >> 1) & 1);
+                mbar_arrive_cluster_relaxed(lead_tp + ab * 8);
+            }
+        }
         // ---- MMA issuer (the pair's leader): the whole warp runs the loop,
         // one elected lane issues (FWD_ELECT)
         if (crank == 0 && (FWD_ELECT || lane == 0)) {
@@ -535,6 +560,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                 const int ab = PS ? (tc & 1) : 0;
                 const uint32_t tph = PS ? (((tc >> 1) & 1) ^ 1) : ((tc & 1) ^ 1);
                 mbar_wait(&tempty[ab], tph);
+                if (PAIR) mbar_wait(&tempty_p[ab], tph);
                 tc_fence_after();
                 const uint32_t dacc = PS ? tmem + ab * 256 : dcol;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -648,10 +674,7 @@ __global__ void __launch_bounds__(FTS_THREADS, 1)
                     if (hh == 1) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) {
-                            if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[ab]), 0));
-                            else mbar_arrive(&tempty[ab]);
-                        }
+                        if (lane == 0) mbar_arrive(&tempty[ab]);  // (PAIR: relayed)
                     }
                     if (!(P.exp_flags & 4)) {
 #pragma unroll
