@@ -23,20 +23,25 @@
 // issuer (elected lane); 2-3 input prep (d'); 4-7 generators (one per TMEM
 // lane quarter, 32 samples each); 8-15 epilogue (two per lane quarter).
 //
-// CL = 2: a CTA pair (cta_group::2) on two x tiles of the same frame, y
-// tile and k range: M = 256 pair MMAs (each CTA's generated A in its own
-// TMEM), the static B tiles split over the pair along N (each CTA's shared
-// memory holds N/2 of the rows), so the B traffic into each SM's shared
-// memory (TMA writes and MMA reads) halves.  The leader (rank 0) issues the
-// MMAs once both CTAs' generators filled the A stage: the peer's
-// generators arrive on their own `gen`, the peer's idle MMA warp relays
-// that to the leader's `genp` (one remote arrive per K block, off the
-// generators' path); both CTAs' B loads complete on the leader's `bfull`
-// (cta_group::2 TMA); MMA commits are multicast onto both CTAs' `bempty`,
-// `aempty` and `acc_full`; both epilogues release the accumulator on the
-// leader's `acc_empty`.  The running sums of columns >= 128 live in shared
-// memory (freed by the halved B stages), which leaves TMEM to the
-// accumulator and four A stages.
+// CL = 2 (the form every wide plan takes: the x-tile count is always even):
+// a CTA pair (cta_group::2) on two x tiles of the same frame, y tile and k
+// range: M = 256 pair MMAs (each CTA's generated A in its own TMEM), the
+// static B tiles split over the pair along N (each CTA's shared memory
+// holds N/2 of the rows), so the B traffic into each SM's shared memory
+// (TMA writes and MMA reads) halves.  Synchronisation across the pair:
+//   - both CTAs' B loads complete on the leader's `bfull` (cta_group::2
+//     TMA, the leader arms it for both CTAs' bytes);
+//   - the leader's MMA commits are multicast onto both CTAs' `bempty`,
+//     `aempty` and `acc_full`;
+//   - every warp arrives on CTA-local barriers (`gen`, `acc_empty`); the
+//     peer's otherwise idle MMA warp acquires those and relays them to
+//     the leader's `genp` / `acc_emptyp` with relaxed cluster-scope
+//     arrives (a release.cluster arrive costs ~2000 cycles, measured).
+// The running sums of columns >= 128 live in shared memory (float4
+// [col / 4][lane], in the space the halved B stages free), which leaves
+// TMEM to the accumulator and four A stages:
+//   TMEM (CL = 2): [0, N) D | [N, N + 64 NA) A stages.
+// CL = 1 remains as the single-CTA form (debug builds: CSR_ADJW_CL=1).
 #pragma once
 
 #include "tc_adjoint.cuh"
