@@ -48,9 +48,9 @@ METRIC = "ADMM iters/s"
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of each NUDFT GEMM
 # (the roofline reports the dominant one), from one `ncu --set full`
 # capture each (cold cache: the factors come from HBM): config 1
-# profiles/r02g_ncu_gemm_c1.txt, config 4 profiles/r02g_ncu_gemm_c4.txt
-TRAFFIC = {1: {"forward": 35697920, "adjoint": 35689216 + 1280},
-           4: {"forward": 4372727000 + 89477632, "adjoint": 3741954000 + 38958848}}
+# profiles/r02h_ncu_gemm_c1.txt, config 4 profiles/r02h_ncu_gemm_c4.txt
+TRAFFIC = {1: {"forward": 35698944, "adjoint": 35688704},
+           4: {"forward": 4361151000 + 90105856, "adjoint": 3685549000 + 36485120}}
 
 
 def peaks():
