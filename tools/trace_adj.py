@@ -34,3 +34,10 @@ dt = (ctas[:, 1] - ctas[:, 0]).astype(float)
 dc = (ctas[:, 31] - ctas[:, 30]).astype(float)
 ok = (dt > 0) & (dc > 0)
 print("SM clock during adjoint (MHz): median", np.median(dc[ok] / dt[ok] * 1e3))
+# per-CTA phases: start -> MMA loop done (tr[1]) -> end after the coil combine (tr[28])
+e = ctas[:, 28]
+okp = e > 0
+if okp.any():
+    print("per CTA (us): start->mma done med", np.median((ctas[okp, 1] - ctas[okp, 0]) / 1e3),
+          " mma done->end med", np.median((e[okp] - ctas[okp, 1]) / 1e3),
+          " first start->last end", (e[okp].max() - ctas[okp, 0].min()) / 1e3)
