@@ -37,8 +37,10 @@ struct FwdParams {
 // 128 x 128 x 256 complex tile, MMA floor 12288).  The leader (rank 0)
 // issues the MMAs; both CTAs' TMA loads complete on the leader's `full`
 // barrier (cta_group::2 form); MMA commits are multicast onto both CTAs'
-// `empty` / `tfull` barriers; both CTAs' epilogues release an accumulator
-// on the leader's `tempty`.  Three 64 KiB stages per CTA.
+// `empty` / `tfull` barriers; each epilogue releases an accumulator on its
+// own CTA's `tempty`, and the peer's idle MMA lane relays the peer's
+// releases to the leader's `tempty_p` with relaxed cluster arrives.  Three
+// 64 KiB stages per CTA.
 constexpr int FWD_PAIR_STAGE = 2 * TC_A_TILE + TC_B_TILE;  // A hi/lo + B hi/lo halves
 constexpr int FWD_PAIR_STAGES = 3;
 static_assert(FWD_PAIR_STAGES * FWD_PAIR_STAGE <= TC_STAGES * TC_FWD_OPS, "pair stages fit");
