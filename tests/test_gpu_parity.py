@@ -76,6 +76,8 @@ def test_operator_random_shapes_vs_direct_sum(cuda):
     (40, 320, 3, 1800),    # two full tiles + a half tile, padded coils
     (32, 200, 16, 1500),   # ny % 128 = 72, 16 coils
     (96, 136, 5, 2048),    # ny % 128 = 8: a mostly empty last tile
+    (40, 160, 4, 1100),    # 9 sample tiles: the single-CTA SS forward (odd, unpadded)
+    (24, 144, 8, 1850),    # 15 sample tiles: padded to 16 for the pair forward
     (64, 64, 32, 3000),    # 32 coils: CP = 32 tensor-core tiles (2 x per adjoint row block)
     (40, 96, 48, 2000),    # > 32 coils: the SIMT kernels
     (24, 20, 66, 700),     # (and 66 coils)
