@@ -7,6 +7,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_micro tools/mma_micro.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cstdlib>
 
 #include "../paper_2006_14080_b200/csrc/sm100.cuh"
 
@@ -629,7 +631,62 @@ void run(unsigned long long *d_out) {
            N, TS ? "TS" : "SS", NACC, cyc, 128 * N / 256, 128.0 * N * 16 / cyc);
 }
 
+// random fp16 in [-1, 1) (realistic operand toggling for the power runs)
+__global__ void k_fill_rand(uint16_t *p, size_t n, unsigned seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned h = (unsigned)i * 2654435761u ^ seed;
+        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+        const float v = (float)(h & 0xFFFFFF) / 8388608.0f - 1.0f;
+        p[i] = __half_as_ushort(__float2half_rn(v));
+    }
+}
+// sustained run of one form: tiles of complex work per second (the caller
+// samples nvidia-smi clocks / power meanwhile)
+template <bool GAUSS, bool PAIR, int NSTG, int NEPI>
+void power_run(unsigned long long *d_out, const uint8_t *g, size_t gbytes, double secs, const char *name) {
+    const int nt = 64;
+    const int smem = PAIR ? NSTG * (32768 + 2 * (GAUSS ? 8192 : 16384)) + 1024
+                          : NSTG * (GAUSS ? 65536 : 98304) + 1024;
+    if (PAIR) cudaFuncSetAttribute(k_cplx2<GAUSS, NSTG, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    else cudaFuncSetAttribute(k_cplx<GAUSS, NSTG, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    int launches = 0;
+    float ms = 0.f;
+    cudaEventRecord(a);
+    while (ms < secs * 1e3) {
+        for (int r = 0; r < 20; ++r, ++launches) {
+            if (PAIR) k_cplx2<GAUSS, NSTG, NEPI><<<148, 64 + 32 * NEPI, smem>>>(nt, g, gbytes, d_out);
+            else k_cplx<GAUSS, NSTG, NEPI><<<148, 64 + 32 * (NEPI > 0 ? NEPI : 0), smem>>>(nt, g, gbytes, d_out);
+        }
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+    }
+    // complex work per launch: 148 SMs x nt tiles of 128 x 128 x 256 complex MACs
+    const double cmacs = 148.0 * nt * 128.0 * 128.0 * 256.0 * launches;
+    printf("POWER %s: %.3f s, %.1f complex TMAC/s (x8 = algorithmic TFLOP/s %.1f)\n", name, ms / 1e3,
+           cmacs / (ms * 1e-3) / 1e12, 8 * cmacs / (ms * 1e-3) / 1e12);
+    fflush(stdout);
+}
+
 int main(int argc, char **argv) {
+    if (argc > 2 && argv[1][0] == 'p') {  // power mode: mma_micro p <form>
+        unsigned long long *d_out;
+        cudaMalloc(&d_out, 148 * 8);
+        uint8_t *g;
+        cudaMalloc(&g, 8 << 20);
+        k_fill_rand<<<148 * 4, 256>>>(reinterpret_cast<uint16_t *>(g), (8 << 20) / 2, 12345u);
+        cudaDeviceSynchronize();
+        const int form = atoi(argv[2]);
+        const double secs = argc > 3 ? atof(argv[3]) : 4.0;
+        if (form == 0) power_run<false, false, 2, 4>(d_out, g, 8 << 20, secs, "DBL single");
+        if (form == 1) power_run<false, true, 3, 4>(d_out, g, 8 << 20, secs, "DBL pair");
+        if (form == 2) power_run<true, false, 3, 4>(d_out, g, 8 << 20, secs, "GAUSS single");
+        if (form == 3) power_run<true, true, 4, 4>(d_out, g, 8 << 20, secs, "GAUSS pair");
+        return 0;
+    }
     const bool only_cplx = argc > 1;
     unsigned long long *d_out;
     cudaMalloc(&d_out, 148 * 8);
