@@ -586,6 +586,38 @@ def test_admm_shapes_vs_oracle(cuda, T, nx, ny, C, m):
     assert [r["cg_iterations"] for r in rep.iterations] == [5] * 4
 
 
+def test_admm_early_cg_stop_on_pair_kernels(cuda):
+    # ny > 128 selects the CTA-pair SS forward and the CTA-pair wide adjoint;
+    # a reachable CG tolerance gates them off mid-loop (their prefetched
+    # stages must land before the CTAs leave), then the next ADMM iteration
+    # runs them again.  Checked against the f64 restatement with the same
+    # early stops.
+    rng = np.random.default_rng(77)
+    nx, ny, C, m = 32, 160, 4, 1500
+    coords = rng.uniform(-0.5, 0.4999, size=(m, 2))
+    sens = random_complex(rng, (C, nx, ny)) * 0.5
+    truth = random_complex(rng, (nx, ny))
+    data = O.Operator(coords, sens).forward(truth)
+    base = dict(lam=1e-3, beta=1e-2, admm_rtol=1e-150, admm_max_iters=3, cg_atol=1e-150)
+    _, rep3 = P.admm_reconstruct(_dataset(coords, data), sens,
+                                 P.ReconParams(cg_max_iters=3, **base), compute_objectives=False)
+    # a tolerance the first CG solve reaches after about three iterations
+    atol = float(np.sqrt(rep3.iterations[0]["cg_final_residual_sq"])) * 1.05
+    kw = dict(base, cg_atol=atol, cg_max_iters=8)
+    img, rep = P.admm_reconstruct(_dataset(coords, data), sens, P.ReconParams(**kw),
+                                  compute_objectives=False)
+    its = [r["cg_iterations"] for r in rep.iterations]
+    assert len(its) == 3 and min(its) < 8, its
+    for r in rep.iterations:
+        assert r["cg_iterations"] == 8 or r["cg_final_residual_sq"] <= atol ** 2
+    ref, orecs = O.admm(data, coords, sens, O.Params(**kw))
+    err = rel_err(img, ref)
+    if [r["cg_iterations"] for r in orecs] == its:
+        assert err <= IMG_TOL, err
+    else:  # a stop decided by rounding at the threshold
+        assert err <= 5e-2, err
+
+
 def test_admm_early_stop_semantics(cuda):
     # reachable tolerances exercise the device loop guards: CG stops when
     # tau <= atol^2 (solver.py:112), ADMM when alpha <= rtol^2 or at the cap
