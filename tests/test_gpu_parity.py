@@ -101,6 +101,36 @@ def test_operator_tile_shapes_vs_oracle(cuda, nx, ny, nc, m):
     assert ea <= OP_TOL, ea
 
 
+def test_operator_random_pair_shapes_vs_oracle(cuda):
+    # random shapes through the CTA-pair kernels: ny in (128, 256] (wide pair
+    # adjoint, N = 160 ... 256 and its shared-memory sums; SS pair forward,
+    # odd sample-tile counts padded or single-CTA) and ny <= 128 (persistent
+    # pair forward with split tiles, narrow adjoint), 1-16 coils, one or two
+    # frames; forward and adjoint vs the f64 separable restatement
+    rng = np.random.default_rng(4242)
+    for i in range(16):
+        T = int(rng.integers(1, 3))
+        nx = int(rng.integers(8, 49))
+        ny = int(rng.integers(129, 257)) if i % 4 else int(rng.integers(40, 129))
+        nc, m = int(rng.integers(1, 17)), int(rng.integers(600, 2400))
+        coords = rng.uniform(-0.5, 0.4999, size=(T * m, 2))
+        sens = random_complex(rng, (nc, nx, ny))
+        img = random_complex(rng, (T, nx, ny))
+        y = random_complex(rng, (T * m, nc))
+        op = P.DftOperator.build(coords, P.ImageGrid(nx, ny), sens.astype(np.complex64),
+                                 n_frames=T)
+        assert op.info()["gemm_path"] == "tcgen05"
+        got_f = op.forward(img.astype(np.complex64) if T > 1 else img[0].astype(np.complex64))
+        got_a = op.adjoint(y.astype(np.complex64))
+        for t in range(T):
+            p0, p1 = O.build_factors(coords[t * m:(t + 1) * m], nx, ny, "double")
+            ef = rel_err(np.asarray(got_f)[t * m:(t + 1) * m], O.forward_sep(p0, p1, sens, img[t]))
+            ga = np.asarray(got_a)[t] if T > 1 else np.asarray(got_a)
+            ea = rel_err(ga, O.adjoint_sep(p0, p1, sens, y[t * m:(t + 1) * m]))
+            assert ef <= OP_TOL, (T, nx, ny, nc, m, ef)
+            assert ea <= OP_TOL, (T, nx, ny, nc, m, ea)
+
+
 def test_adjointness(cuda):
     # test_operators.py:129-140 / criterion 2, in fp32
     rng = np.random.default_rng(44)
