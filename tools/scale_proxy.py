@@ -1,5 +1,5 @@
-"""Single-GPU proxy of one rank of a P-GPU frame-sharded run (BASELINE
-config 3 / 4): the first T/P frames of the config as their own problem,
+"""Single-GPU proxy of one rank of a P-GPU sharded run.  2-D+t configs
+(3 / 4): the first T/P frames of the config as their own problem,
 frame-shard mode with a one-rank NCCL communicator attached, so the plan
 takes exactly the code path of a rank of the P-GPU run (frame-split CG
 kernels, halo all-gather, fp64 scalar allreduces, its GEMM grids for T/P
@@ -7,6 +7,9 @@ frames) — only the NCCL transfers go to self instead of over NVLink.
 Device time of K ADMM iterations (CUDA events, L2 flushed between
 iterations, as bench.py).  The P-GPU rate is bounded by one rank's rate,
 so  efficiency(P) ~= rate(T/P frames) / (P * rate(T frames, 1 GPU)).
+Static configs (0-2): the rank's coils (coil shard, >= 4 coils per rank) or
+its 1/P of the samples (sample split), with the shard mode's per-CG-iteration
+image allreduce through the one-rank communicator.
 
     python tools/scale_proxy.py [config=4] [steps=10]
 prints one JSON line per P in 1, 2, 4, 8 plus the plain 1-GPU run."""
@@ -28,12 +31,17 @@ from bench import ClockSampler, input_encoder  # noqa: E402
 from harness.configs import make_problem  # noqa: E402
 
 
-def rate(prob, frames, steps, shard, collective, dev):
+def rate(prob, frames, steps, shard, collective, dev, samples=None, coils=None):
     m = prob.coords.shape[0] // prob.n_frames
     coords, data = prob.coords[:frames * m], prob.data[:frames * m]
+    sens = prob.sens
+    if samples is not None:  # static sample split: this rank's run of samples
+        coords, data = coords[:samples], data[:samples]
+    if coils is not None:    # static coil split: this rank's coils
+        sens, data = sens[:coils], data[:, :coils]
     traj = P.Trajectory(coords, coords.shape[0], 1)
     ds = P.KSpaceDataset(data, traj, n_frames=frames)
-    sh = _Shard(ds, prob.sens, 1, "auto", dev, shard=shard, collective=collective)
+    sh = _Shard(ds, sens, 1, "auto", dev, shard=shard, collective=collective)
     op, lib = sh.op, _native.load()
 
     def run(n, iter_ms=None, flush=None):
@@ -75,11 +83,22 @@ def main():
     print(json.dumps({"config": cfg, "mode": "1 GPU, no communicator", "frames": T,
                       "iters_per_s": r1, "kernels_per_iter": k1, "clocks": c1}), flush=True)
     for p in (1, 2, 4, 8):
-        if T % p:
-            continue
-        r, k, c = rate(prob, T // p, steps, "frame", "nccl", dev)
-        print(json.dumps({"config": cfg, "mode": f"one rank of {p} (frame shard, 1-rank NCCL)",
-                          "frames": T // p, "iters_per_s": r, "kernels_per_iter": k,
+        if T > 1:
+            if T % p:
+                continue
+            r, k, c = rate(prob, T // p, steps, "frame", "nccl", dev)
+            what, size = "frame shard", {"frames": T // p}
+        else:
+            # bench.py's static split: coils while >= 4 per rank, else samples
+            C, M = prob.n_coils, prob.coords.shape[0]
+            if C // p >= 4:
+                r, k, c = rate(prob, 1, steps, "coil", "nccl", dev, coils=C // p)
+                what, size = "coil shard", {"coils": C // p}
+            else:
+                r, k, c = rate(prob, 1, steps, "split", "nccl", dev, samples=M // p)
+                what, size = "sample split", {"samples": M // p}
+        print(json.dumps({"config": cfg, "mode": f"one rank of {p} ({what}, 1-rank NCCL)", **size,
+                          "iters_per_s": r, "kernels_per_iter": k,
                           "proxy_efficiency_vs_1gpu": r / (p * r1), "clocks": c}), flush=True)
 
 
